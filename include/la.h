@@ -1,0 +1,162 @@
+/*
+ * la.h -- C ABI of the B200-native fp32-accurate GEMM (after arXiv 1306.6192).
+ *
+ * The one operation is the Cauchy product of PAPER.md P:47 (section
+ * "Implementacje algorytmow"):
+ *
+ *     c_ij = sum_{r=1..m} a_ir * b_rj,   1 <= i <= n, 1 <= j <= p,
+ *
+ * for dense ROW-MAJOR single-precision matrices: A is n x m (element (i,r) at
+ * A[i*m + r]), B is m x p (B[r*p + j]), C is n x p (C[i*p + j]) -- the
+ * indexing of Listing 1 and of Listing 4's write-back.
+ * There is no alpha/beta and no accumulate-into-C: C is overwritten.
+ *
+ * Conventions for every function:
+ *  - Returns la_status; never throws or aborts across the ABI.  On failure a
+ *    thread-local detail string is available from la_last_error().
+ *  - Pointers named d_* are DEVICE pointers on the device given to la_init()
+ *    (e.g. torch tensor data_ptr()); pointers named h_* are HOST pointers.
+ *    Device operands are caller-owned; the library owns only its workspace
+ *    (stream-ordered, from a CUDA memory pool), its TMA descriptors and, after
+ *    la_comm_init, one NCCL communicator.  C must not overlap A or B.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device work is enqueued on it and the call returns without a host sync;
+ *    asynchronous kernel faults surface at the caller's next synchronisation
+ *    (or as LA_ERR_CUDA from a later la_* call).  la_gemm does no host
+ *    synchronisation and allocates with cudaMallocAsync, so it may be captured
+ *    into a CUDA graph.
+ *  - Sizes are int64_t; all index arithmetic on the device is 64-bit
+ *    (n*p = 2^32 at n = 65536 overflows Listing 4's 32-bit `int c`).
+ *
+ * Numerics (BASELINE.json north_star):
+ *  - LA_MODE_3XTF32 (default): a = hi + lo with hi = tf32 round-to-nearest
+ *    (ties away) of a and lo = a - hi; c = sum(hi*hi' + hi*lo' + lo*hi') on
+ *    the tcgen05 tensor pipe with fp32 accumulation.  Contract:
+ *    |c - c_ref| <= 2^-20 * sum_r |a_ir||b_rj| per element, and value-exact
+ *    (==) on integer-valued inputs whose partial sums stay below 2^24.
+ *  - LA_MODE_TF32: one pass on hi only; contract 2^-9 * sum_r |a_ir||b_rj|.
+ *  - Inputs must be finite; non-finite inputs are out of contract.
+ */
+#ifndef LA_H_
+#define LA_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LA_API __attribute__((visibility("default")))
+#else
+#define LA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LA_OK = 0,
+    LA_ERR_INVALID_VALUE = 1,   /* bad dimension (<= 0), NULL or aliased pointer, bad mode/option */
+    LA_ERR_NOT_INITIALIZED = 2, /* la_init (or la_comm_init for *_multi) has not been called */
+    LA_ERR_UNSUPPORTED = 3,     /* device is not sm_100 (B200), or a shape the multi-GPU path rejects */
+    LA_ERR_OUT_OF_MEMORY = 4,   /* workspace / host staging allocation failed */
+    LA_ERR_CUDA = 5,            /* a CUDA runtime/driver call failed (detail in la_last_error) */
+    LA_ERR_NCCL = 6             /* an NCCL call failed (detail in la_last_error) */
+} la_status;
+
+typedef enum {
+    LA_MODE_3XTF32 = 0, /* fp32-accurate: three TF32 tensor-core passes (default) */
+    LA_MODE_TF32 = 1    /* one TF32 pass, ~2^-10 relative per product */
+} la_mode;
+
+typedef enum {
+    /* K elements accumulated in tensor memory before the partial sum is added
+     * into an fp32 register running sum (round-to-nearest).  0 = never (the whole
+     * K range accumulates in TMEM).  Rounded up to a multiple of 32.  Default:
+     * chosen from the accumulator-rounding probe, see DESIGN.md. */
+    LA_OPT_PROMOTE_K = 0,
+    /* Upper bound on the number of SMs the GEMM kernel occupies (0 = all).  The
+     * multi-GPU path uses it to leave SMs for NCCL. */
+    LA_OPT_MAX_SMS = 1,
+    /* Number of N-panels B is broadcast in by la_gemm_multi (>= 1). */
+    LA_OPT_PANELS = 2
+} la_option;
+
+/* Bind the calling thread's library state to CUDA device `device`, check that it
+ * is compute capability 10.0 (sm_100, B200) and set up the workspace pool.
+ * Idempotent for the same device.  Errors: INVALID_VALUE (no such device),
+ * UNSUPPORTED (not sm_100), CUDA. */
+LA_API la_status la_init(int device);
+
+/* Process-wide arithmetic mode for subsequent calls (default LA_MODE_3XTF32).
+ * Errors: INVALID_VALUE (unknown mode). */
+LA_API la_status la_set_mode(la_mode mode);
+
+/* Set / get a tuning option (see la_option).  Errors: INVALID_VALUE. */
+LA_API la_status la_set_option(la_option option, int64_t value);
+LA_API la_status la_get_option(la_option option, int64_t *value);
+
+/* C = A . B on one GPU, enqueued on `stream` (Listing 4's role).
+ *   n, m, p   : dimensions, each >= 1;
+ *   d_A       : n x m row-major fp32, device;  d_B : m x p row-major fp32, device;
+ *   d_C       : n x p row-major fp32, device, written exactly once per element.
+ * Work: one split pass over A and over B into a library workspace, then one
+ * persistent tcgen05 GEMM kernel.  Errors: NOT_INITIALIZED, INVALID_VALUE
+ * (dims, NULL, C overlapping A or B), OUT_OF_MEMORY, CUDA. */
+LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B,
+                  float *d_C, void *stream);
+
+/* End-to-end variant on HOST buffers (the paper's host flow):
+ * copies h_A and h_B to the device, computes, copies C back into h_C and
+ * synchronises `stream` before returning.  Host buffers may be pageable or
+ * pinned (pinned is faster).  Device staging is library-owned and reused
+ * across calls.  Errors: as la_gemm. */
+LA_API la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B,
+                       float *h_C, void *stream);
+
+/* ---- multi-GPU (one process per GPU, SPMD) ------------------ */
+
+/* Rank 0 writes a 128-byte NCCL unique id into out128; the caller distributes
+ * it (e.g. torch.distributed broadcast).  Errors: INVALID_VALUE, NCCL. */
+LA_API la_status la_get_unique_id(void *out128);
+
+/* Create this rank's communicator (rank in [0, ngpu)).  Requires la_init.
+ * Errors: NOT_INITIALIZED, INVALID_VALUE, NCCL. */
+LA_API la_status la_comm_init(const void *uid128, int rank, int ngpu);
+
+/* Row-sharded product over the communicator:
+ *   rank r owns rows [r*n/g, (r+1)*n/g) of A and C (g = ngpu);
+ *   d_A_local : (rows_r x m) row-major fp32;
+ *   d_B       : m x p on rank `root` (ignored, may be NULL, elsewhere) --
+ *               broadcast with ncclBroadcast in N-panels overlapped with the
+ *               GEMM on the panels already received;
+ *   d_C_local : (rows_r x p) row-major fp32;
+ *   d_C_full  : NULL, or n x p: if given, C is all-gathered (ncclAllGather)
+ *               into it on every rank (requires n % g == 0).
+ * All ranks pass identical n, m, p, root, ngpu.  Every output element is
+ * accumulated in the same order as la_gemm, so results are bitwise identical
+ * to the single-GPU path.  Errors: NOT_INITIALIZED, INVALID_VALUE (ngpu !=
+ * communicator size, dims), UNSUPPORTED (C_full with n % g != 0), NCCL, CUDA. */
+LA_API la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
+                        const float *d_B, float *d_C_local, float *d_C_full, int root,
+                        int ngpu, void *stream);
+
+/* Rows owned by `rank` of g: [*row0, *row0 + *rows).  Pure host arithmetic. */
+LA_API la_status la_shard_rows(int64_t n, int rank, int ngpu, int64_t *row0, int64_t *rows);
+
+/* Release workspace pools, staging buffers and the communicator.  The library
+ * may be re-initialised afterwards. */
+LA_API la_status la_finalize(void);
+
+/* Static description of a status code. */
+LA_API const char *la_status_string(la_status s);
+
+/* Thread-local detail message of the last failing call on this thread ("" if none). */
+LA_API const char *la_last_error(void);
+
+/* Number of kernels the last la_gemm / la_gemm_multi call launched. */
+LA_API int la_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LA_H_ */

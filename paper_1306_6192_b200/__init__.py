@@ -1,0 +1,219 @@
+"""Python binding of the C ABI in include/la.h (argument marshalling only).
+
+Every step of the product runs in the CUDA kernels of ``libla.so``; this module
+only converts torch tensors / numpy arrays to pointers and status codes to
+exceptions.  There is no CPU fallback: if the shared library is missing the
+import of the binding fails loudly (build it with ``__graft_entry__.build()``
+or ``python paper_1306_6192_b200/_build.py``).
+
+    import torch, paper_1306_6192_b200 as la
+    la.init(0)
+    C = la.gemm(A, B)          # A: n x m, B: m x p, float32 CUDA tensors
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libla.so")
+
+LA_OK, LA_ERR_INVALID_VALUE, LA_ERR_NOT_INITIALIZED, LA_ERR_UNSUPPORTED, \
+    LA_ERR_OUT_OF_MEMORY, LA_ERR_CUDA, LA_ERR_NCCL = range(7)
+MODES = {"3xtf32": 0, "tf32": 1}
+OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2}
+
+# every symbol include/la.h declares (checked by tests/test_abi.py)
+EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
+           "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
+           "la_status_string", "la_last_error", "la_last_launch_count")
+
+
+class LaError(RuntimeError):
+    def __init__(self, status: int, func: str, detail: str):
+        self.status = status
+        super().__init__(f"{func}: {_lib.la_status_string(status).decode()} ({detail})")
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    i64, vp, st = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+    sig = {
+        "la_init": ([ctypes.c_int], st),
+        "la_set_mode": ([ctypes.c_int], st),
+        "la_set_option": ([ctypes.c_int, i64], st),
+        "la_get_option": ([ctypes.c_int, ctypes.POINTER(i64)], st),
+        "la_gemm": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_gemm_host": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_get_unique_id": ([vp], st),
+        "la_comm_init": ([vp, ctypes.c_int, ctypes.c_int], st),
+        "la_gemm_multi": ([i64, i64, i64, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp], st),
+        "la_shard_rows": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], st),
+        "la_finalize": ([], st),
+        "la_status_string": ([ctypes.c_int], ctypes.c_char_p),
+        "la_last_error": ([], ctypes.c_char_p),
+        "la_last_launch_count": ([], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes, f.restype = args, res
+    return lib
+
+
+_lib = _load()
+
+
+def _check(status: int, func: str) -> None:
+    if status != LA_OK:
+        raise LaError(status, func, _lib.la_last_error().decode())
+
+
+def status_string(status: int) -> str:
+    return _lib.la_status_string(int(status)).decode()
+
+
+def init(device: int | None = None) -> None:
+    """la_init on `device` (default: torch's current CUDA device)."""
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    _check(_lib.la_init(int(device)), "la_init")
+
+
+def finalize() -> None:
+    _check(_lib.la_finalize(), "la_finalize")
+
+
+def set_mode(mode: str) -> None:
+    """'3xtf32' (default, fp32-accurate) or 'tf32'."""
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {sorted(MODES)}")
+    _check(_lib.la_set_mode(MODES[mode]), "la_set_mode")
+
+
+def set_option(name: str, value: int) -> None:
+    _check(_lib.la_set_option(OPTIONS[name], int(value)), "la_set_option")
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    _check(_lib.la_get_option(OPTIONS[name], ctypes.byref(v)), "la_get_option")
+    return v.value
+
+
+def last_launch_count() -> int:
+    return _lib.la_last_launch_count()
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check_dev(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+        raise TypeError(f"{name} must be a float32 CUDA tensor")
+    if t.dim() != 2 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous 2-D (row-major) matrix")
+
+
+def gemm(A, B, out=None, stream=None):
+    """C = A . B (la_gemm) for float32 CUDA tensors; returns C (n x p)."""
+    import torch
+    _check_dev(A, "A")
+    _check_dev(B, "B")
+    n, m = A.shape
+    m2, p = B.shape
+    if m != m2:
+        raise ValueError(f"inner dimension mismatch: {tuple(A.shape)} x {tuple(B.shape)}")
+    if out is None:
+        out = torch.empty((n, p), dtype=torch.float32, device=A.device)
+    else:
+        _check_dev(out, "out")
+        if tuple(out.shape) != (n, p):
+            raise ValueError("out has the wrong shape")
+    _check(_lib.la_gemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_gemm")
+    return out
+
+
+def gemm_raw(n, m, p, a_ptr, b_ptr, c_ptr, stream_ptr=0):
+    """la_gemm on raw device pointers (no checks beyond the library's)."""
+    _check(_lib.la_gemm(n, m, p, a_ptr, b_ptr, c_ptr, ctypes.c_void_p(stream_ptr)), "la_gemm")
+
+
+def gemm_host(A, B, out=None, stream=None):
+    """End-to-end la_gemm_host on host float32 arrays (numpy, or CPU tensors,
+    pinned or not); copies in, computes, copies out, synchronises."""
+    import torch
+    def arr(x):
+        if isinstance(x, torch.Tensor):
+            if x.device.type != "cpu" or x.dtype != torch.float32 or not x.is_contiguous():
+                raise TypeError("host tensors must be contiguous float32 on the CPU")
+            return x, x.data_ptr(), tuple(x.shape)
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        return x, x.ctypes.data, x.shape
+    A, pa, sa = arr(A)
+    B, pb, sb = arr(B)
+    n, m = sa
+    m2, p = sb
+    if m != m2:
+        raise ValueError("inner dimension mismatch")
+    if out is None:
+        out = np.empty((n, p), dtype=np.float32)
+    out, pc, sc = arr(out)
+    if tuple(sc) != (n, p):
+        raise ValueError("out has the wrong shape")
+    _check(_lib.la_gemm_host(n, m, p, pa, pb, pc, _stream_ptr(stream)), "la_gemm_host")
+    return out
+
+
+def shard_rows(n: int, rank: int, ngpu: int):
+    """(row0, rows) owned by `rank` of `ngpu` (la_shard_rows)."""
+    r0, r = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.la_shard_rows(int(n), int(rank), int(ngpu), ctypes.byref(r0), ctypes.byref(r)), "la_shard_rows")
+    return r0.value, r.value
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.la_get_unique_id(buf), "la_get_unique_id")
+    return buf.raw
+
+
+def comm_init(uid: bytes, rank: int, ngpu: int) -> None:
+    if len(uid) != 128:
+        raise ValueError("the NCCL unique id is 128 bytes")
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(_lib.la_comm_init(buf, int(rank), int(ngpu)), "la_comm_init")
+
+
+def comm_init_from_process_group(group=None) -> None:
+    """Bootstrap the library's NCCL communicator over an initialised
+    torch.distributed process group (rank 0 creates the id, broadcast over the
+    group, every rank calls la_comm_init)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = get_unique_id() if rank == 0 else bytes(128)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, src=0, group=group)
+    comm_init(bytes(t.cpu().tolist()), rank, world)
+
+
+def gemm_multi(n, m, p, A_local, B, C_local, C_full=None, root=0, ngpu=1, stream=None):
+    """la_gemm_multi: row-sharded product; B is read on `root` only."""
+    _check_dev(A_local, "A_local")
+    _check_dev(C_local, "C_local")
+    b = 0 if B is None else B.data_ptr()
+    cf = 0 if C_full is None else C_full.data_ptr()
+    _check(_lib.la_gemm_multi(n, m, p, A_local.data_ptr(), b, C_local.data_ptr(), cf, int(root), int(ngpu),
+                              _stream_ptr(stream)), "la_gemm_multi")
+    return C_full if C_full is not None else C_local

@@ -1,0 +1,403 @@
+// la.cu -- host side of the C ABI declared in include/la.h (single-GPU path).
+//
+// la_gemm(n, m, p, A, B, C, stream) enqueues, on the caller's stream:
+//   1. K1 split of A  -> A_hi, A_lo   (n x mp, row-major, K-major for UMMA)
+//   2. K1 split of B  -> Bt_hi, Bt_lo (p x mp, B transposed to K-major)
+//   3. K2 persistent tcgen05 GEMM reading the four operands through TMA
+// with the workspace taken from (and returned to) a CUDA memory pool in stream
+// order, so the call never synchronises the host and can be graph-captured.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "gemm_sm100.cuh"
+#include "la.h"
+#include "la_internal.h"
+#include "split.cuh"
+
+namespace la {
+
+thread_local std::string g_last_error;
+State g_state;
+std::mutex g_mutex;
+
+la_status fail(la_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+la_status cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    return fail(LA_ERR_CUDA, "%s failed: %s (%s) at %s:%d", what, cudaGetErrorName(e),
+                cudaGetErrorString(e), file, line);
+}
+
+// Tuned kernel configurations.
+constexpr int kBN = 128;
+constexpr int kStages3 = 3;  // 3 x 64 KB stages for 3xTF32
+constexpr int kStages1 = 6;  // 6 x 32 KB stages for plain TF32
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D fp32 tensor map over a rows x cols row-major buffer (cols % 4 == 0),
+// box = box_rows x 32 columns, 128-byte swizzle, OOB elements read as zero.
+static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols,
+                           int box_rows) {
+    auto enc = get_encoder();
+    if (!enc) return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld", (int)r,
+                    (long long)rows, (long long)cols);
+    return LA_OK;
+}
+
+size_t operands_bytes(int64_t n, int64_t m, int64_t p, int passes) {
+    const int64_t mp = pad_k(m);
+    return (size_t)((n + p) * mp) * sizeof(float) * (passes == 3 ? 2 : 1) + 1024;
+}
+
+Operands operands_carve(void *ws, int64_t n, int64_t m, int64_t p, int passes) {
+    Operands o;
+    o.mp = pad_k(m);
+    o.passes = passes;
+    float *base = static_cast<float *>(ws);
+    // every buffer 16-byte aligned (n*mp and p*mp are multiples of 4 floats)
+    o.a_hi = base;
+    o.b_hi = o.a_hi + n * o.mp;
+    o.a_lo = passes == 3 ? o.b_hi + p * o.mp : o.a_hi;
+    o.b_lo = passes == 3 ? o.a_lo + n * o.mp : o.b_hi;
+    return o;
+}
+
+la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cudaStream_t st, int *launches) {
+    if (m % 4 == 0) {
+        const int64_t count4 = n * m / 4;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, (int64_t)g_state.sms * 8));
+        if (ops.passes == 3)
+            split_rows_vec4_kernel<3><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
+                                                              reinterpret_cast<float4 *>(ops.a_hi),
+                                                              reinterpret_cast<float4 *>(ops.a_lo), count4);
+        else
+            split_rows_vec4_kernel<1><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
+                                                              reinterpret_cast<float4 *>(ops.a_hi),
+                                                              reinterpret_cast<float4 *>(ops.a_lo), count4);
+    } else {
+        dim3 grid((unsigned)std::min<int64_t>((ops.mp + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
+        if (ops.passes == 3)
+            split_rows_kernel<3><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp);
+        else
+            split_rows_kernel<1><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp);
+    }
+    (*launches)++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "split_a launch", __FILE__, __LINE__);
+    return LA_OK;
+}
+
+la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb, const Operands &ops,
+                  cudaStream_t st, int *launches) {
+    dim3 grid((unsigned)((pc + 31) / 32), (unsigned)((ops.mp + 31) / 32));
+    if (grid.y > 65535) return fail(LA_ERR_UNSUPPORTED, "m = %lld too large for the split grid", (long long)m);
+    const float *b = B;  // B points at column j0 of the source matrix
+    float *hi = ops.b_hi + j0 * ops.mp, *lo = ops.b_lo + j0 * ops.mp;
+    if (ops.passes == 3)
+        split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
+    else
+        split_transpose_kernel<1><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
+    (*launches)++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "split_b launch", __FILE__, __LINE__);
+    return LA_OK;
+}
+
+template <int BN, int STAGES, int PASSES>
+static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C,
+                             int64_t ldc, int max_sms, cudaStream_t st, int *launches) {
+    using Cfg = GemmCfg<BN, STAGES, PASSES>;
+    CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+    la_status s;
+    const float *bh = ops.b_hi + j0 * ops.mp, *bl = ops.b_lo + j0 * ops.mp;
+    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, BM)) != LA_OK) return s;
+    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, BN)) != LA_OK) return s;
+    if (PASSES == 3) {
+        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, BM)) != LA_OK) return s;
+        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, BN)) != LA_OK) return s;
+    } else {
+        ta_lo = ta_hi;
+        tb_lo = tb_hi;
+    }
+    GemmArgs args;
+    args.C = C + j0;
+    args.n = n;
+    args.p = pc;
+    args.ldc = ldc;
+    args.num_kb = (int32_t)((m + BK - 1) / BK);
+    const int64_t pk = g_state.promote_k;
+    args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + BK - 1) / BK);
+    if (args.kc > args.num_kb) args.kc = args.num_kb;
+    args.tiles_m = (int32_t)((n + BM - 1) / BM);
+    args.tiles_n = (int32_t)((pc + BN - 1) / BN);
+    args.group_m = 16;
+    const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
+    int sms = g_state.sms;
+    if (max_sms > 0) sms = std::min(sms, max_sms);
+    const int grid = (int)std::min<int64_t>(tiles, sms);
+
+    auto kern = gemm_tf32_sm100_kernel<BN, STAGES, PASSES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)", __FILE__, __LINE__);
+        attr_set = true;
+    }
+    kern<<<grid, NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, args);
+    (*launches)++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
+    return LA_OK;
+}
+
+la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
+                   int max_sms, cudaStream_t st, int *launches) {
+    if (ops.passes == 3) return launch_gemm<kBN, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+    return launch_gemm<kBN, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+}
+
+la_status validate_gemm(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const float *C) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (n <= 0 || m <= 0 || p <= 0)
+        return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1 (n=%lld m=%lld p=%lld)", (long long)n,
+                    (long long)m, (long long)p);
+    if (n > (int64_t)1 << 31 || m > (int64_t)1 << 31 || p > (int64_t)1 << 31)
+        return fail(LA_ERR_UNSUPPORTED, "dimension exceeds 2^31 (TMA coordinates are int32)");
+    if (!A || !B || !C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
+    auto overlap = [](const void *x, int64_t xb, const void *y, int64_t yb) {
+        const char *a = (const char *)x, *b = (const char *)y;
+        return a < b + yb && b < a + xb;
+    };
+    const int64_t ab = n * m * 4, bb = m * p * 4, cb = n * p * 4;
+    if (overlap(C, cb, A, ab) || overlap(C, cb, B, bb))
+        return fail(LA_ERR_INVALID_VALUE, "C overlaps A or B");
+    return LA_OK;
+}
+
+// C (n x p, row stride ldc) = A (n x m) . B (m x p), one GPU.
+static la_status gemm_impl(int64_t n, int64_t m, int64_t p, const float *A, const float *B, float *C, int64_t ldc,
+                           cudaStream_t st, int *launches) {
+    const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
+    const size_t bytes = operands_bytes(n, m, p, passes);
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&ws, bytes, g_state.pool, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LA_ERR_OUT_OF_MEMORY, "workspace of %zu bytes: %s", bytes, cudaGetErrorString(e));
+    }
+    const Operands ops = operands_carve(ws, n, m, p, passes);
+    la_status s = split_a(n, m, A, ops, st, launches);
+    if (s == LA_OK) s = split_b(m, 0, p, B, p, ops, st, launches);
+    if (s == LA_OK) s = gemm_run(n, m, 0, p, ops, C, ldc, (int)g_state.max_sms, st, launches);
+    e = cudaFreeAsync(ws, st);
+    if (s == LA_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);
+    return s;
+}
+
+}  // namespace la
+
+using namespace la;
+
+#define LA_CK(call)                                                          \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+extern "C" {
+
+la_status la_init(int device) {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    g_last_error.clear();
+    if (g_state.initialized) {
+        if (device == g_state.device) {
+            LA_CK(cudaSetDevice(device));
+            return LA_OK;
+        }
+        return fail(LA_ERR_INVALID_VALUE, "already initialised on device %d", g_state.device);
+    }
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount", __FILE__, __LINE__);
+    if (device < 0 || device >= count) return fail(LA_ERR_INVALID_VALUE, "no CUDA device %d (%d present)", device, count);
+    LA_CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    LA_CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(LA_ERR_UNSUPPORTED, "device %d is sm_%d%d (%s); this library is built for sm_100a (B200)",
+                    device, prop.major, prop.minor, prop.name);
+    cudaMemPoolProps pp;
+    memset(&pp, 0, sizeof pp);
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    LA_CK(cudaMemPoolCreate(&g_state.pool, &pp));
+    uint64_t thr = UINT64_MAX;
+    LA_CK(cudaMemPoolSetAttribute(g_state.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_state.device = device;
+    g_state.sms = prop.multiProcessorCount;
+    if (const char *env = getenv("LA_PROMOTE_K")) g_state.promote_k = atoll(env);
+    g_state.initialized = true;
+    return LA_OK;
+}
+
+la_status la_set_mode(la_mode mode) {
+    if (mode != LA_MODE_3XTF32 && mode != LA_MODE_TF32) return fail(LA_ERR_INVALID_VALUE, "unknown mode %d", (int)mode);
+    g_state.mode = mode;
+    return LA_OK;
+}
+
+la_status la_set_option(la_option option, int64_t value) {
+    switch (option) {
+        case LA_OPT_PROMOTE_K:
+            if (value < 0) return fail(LA_ERR_INVALID_VALUE, "promote_k must be >= 0");
+            g_state.promote_k = value;
+            return LA_OK;
+        case LA_OPT_MAX_SMS:
+            if (value < 0) return fail(LA_ERR_INVALID_VALUE, "max_sms must be >= 0");
+            g_state.max_sms = value;
+            return LA_OK;
+        case LA_OPT_PANELS:
+            if (value < 1) return fail(LA_ERR_INVALID_VALUE, "panels must be >= 1");
+            g_state.panels = value;
+            return LA_OK;
+    }
+    return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
+}
+
+la_status la_get_option(la_option option, int64_t *value) {
+    if (!value) return fail(LA_ERR_INVALID_VALUE, "NULL value pointer");
+    switch (option) {
+        case LA_OPT_PROMOTE_K: *value = g_state.promote_k; return LA_OK;
+        case LA_OPT_MAX_SMS: *value = g_state.max_sms; return LA_OK;
+        case LA_OPT_PANELS: *value = g_state.panels; return LA_OK;
+    }
+    return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
+}
+
+la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B, float *d_C,
+                  void *stream) {
+    la_status s = validate_gemm(n, m, p, d_A, d_B, d_C);
+    if (s != LA_OK) return s;
+    int launches = 0;
+    s = gemm_impl(n, m, p, d_A, d_B, d_C, p, static_cast<cudaStream_t>(stream), &launches);
+    g_state.last_launches = launches;
+    return s;
+}
+
+la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
+                       void *stream) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
+    if (!h_A || !h_B || !h_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t ab = (size_t)(n * m) * 4, bb = (size_t)(m * p) * 4, cb = (size_t)(n * p) * 4;
+    const size_t need = ab + bb + cb + 3 * 256;
+    if (g_state.staging_bytes < need) {
+        if (g_state.staging) {
+            LA_CK(cudaStreamSynchronize(st));
+            LA_CK(cudaFree(g_state.staging));
+            g_state.staging = nullptr;
+            g_state.staging_bytes = 0;
+        }
+        cudaError_t e = cudaMalloc(&g_state.staging, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(LA_ERR_OUT_OF_MEMORY, "device staging of %zu bytes", need);
+        }
+        g_state.staging_bytes = need;
+    }
+    char *base = static_cast<char *>(g_state.staging);
+    float *dA = reinterpret_cast<float *>(base);
+    float *dB = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256);
+    float *dC = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256 + (bb + 255) / 256 * 256);
+    LA_CK(cudaMemcpyAsync(dA, h_A, ab, cudaMemcpyHostToDevice, st));
+    LA_CK(cudaMemcpyAsync(dB, h_B, bb, cudaMemcpyHostToDevice, st));
+    int launches = 0;
+    la_status s = gemm_impl(n, m, p, dA, dB, dC, p, st, &launches);
+    g_state.last_launches = launches;
+    if (s != LA_OK) return s;
+    LA_CK(cudaMemcpyAsync(h_C, dC, cb, cudaMemcpyDeviceToHost, st));
+    LA_CK(cudaStreamSynchronize(st));
+    return LA_OK;
+}
+
+la_status la_shard_rows(int64_t n, int rank, int ngpu, int64_t *row0, int64_t *rows) {
+    if (n < 0 || ngpu < 1 || rank < 0 || rank >= ngpu || !row0 || !rows)
+        return fail(LA_ERR_INVALID_VALUE, "bad shard query n=%lld rank=%d ngpu=%d", (long long)n, rank, ngpu);
+    const int64_t a = n * rank / ngpu, b = n * (rank + 1) / ngpu;
+    *row0 = a;
+    *rows = b - a;
+    return LA_OK;
+}
+
+la_status la_finalize(void) {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    if (!g_state.initialized) return LA_OK;
+    cudaDeviceSynchronize();
+    la_status s = comm_destroy();
+    if (g_state.staging) cudaFree(g_state.staging);
+    g_state.staging = nullptr;
+    g_state.staging_bytes = 0;
+    if (g_state.pool) cudaMemPoolDestroy(g_state.pool);
+    g_state.pool = nullptr;
+    g_state.initialized = false;
+    g_state.device = -1;
+    return s;
+}
+
+const char *la_status_string(la_status s) {
+    switch (s) {
+        case LA_OK: return "LA_OK";
+        case LA_ERR_INVALID_VALUE: return "LA_ERR_INVALID_VALUE";
+        case LA_ERR_NOT_INITIALIZED: return "LA_ERR_NOT_INITIALIZED";
+        case LA_ERR_UNSUPPORTED: return "LA_ERR_UNSUPPORTED";
+        case LA_ERR_OUT_OF_MEMORY: return "LA_ERR_OUT_OF_MEMORY";
+        case LA_ERR_CUDA: return "LA_ERR_CUDA";
+        case LA_ERR_NCCL: return "LA_ERR_NCCL";
+    }
+    return "LA_ERR_UNKNOWN";
+}
+
+const char *la_last_error(void) { return g_last_error.c_str(); }
+
+int la_last_launch_count(void) { return g_state.last_launches; }
+
+}  // extern "C"

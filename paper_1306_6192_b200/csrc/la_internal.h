@@ -1,0 +1,63 @@
+// la_internal.h -- state and helpers shared by la.cu (single GPU) and multi.cu (NCCL).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "la.h"
+
+namespace la {
+
+struct State {
+    bool initialized = false;
+    int device = -1;
+    int sms = 0;
+    cudaMemPool_t pool = nullptr;
+    la_mode mode = LA_MODE_3XTF32;
+    // Accumulator promotion interval in K elements (0 = whole K in TMEM).
+    // Default decided by the tcgen05 accumulation probe (App. C).
+    int64_t promote_k = 0;
+    int64_t max_sms = 0;
+    int64_t panels = 4;
+    int last_launches = 0;
+    void *staging = nullptr;  // la_gemm_host device staging
+    size_t staging_bytes = 0;
+};
+
+extern State g_state;
+extern std::mutex g_mutex;
+extern thread_local std::string g_last_error;
+
+la_status fail(la_status s, const char *fmt, ...);
+la_status cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+la_status validate_gemm(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const float *C);
+
+// Split operands of one product (layouts in split.cuh).  b rows are the
+// columns of B (Bt is p x mp); a panel of B's columns is a contiguous row range.
+struct Operands {
+    float *a_hi = nullptr, *a_lo = nullptr;  // n x mp
+    float *b_hi = nullptr, *b_lo = nullptr;  // p x mp
+    int64_t mp = 0;
+    int passes = 3;
+};
+
+inline int64_t pad_k(int64_t m) { return (m + 3) / 4 * 4; }
+size_t operands_bytes(int64_t n, int64_t m, int64_t p, int passes);
+Operands operands_carve(void *ws, int64_t n, int64_t m, int64_t p, int passes);
+
+// A (n x m, row stride m) -> ops.a_hi/a_lo
+la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cudaStream_t st, int *launches);
+// B -> rows [j0, j0+pc) of ops.b_hi/b_lo, where B points at column j0 of an
+// m x (>= pc) row-major matrix with row stride ldb
+la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb, const Operands &ops,
+                  cudaStream_t st, int *launches);
+// C[:, j0:j0+pc] (n x pc block of a row-major matrix with row stride ldc) =
+// A . B[:, j0:j0+pc] from split operands; at most max_sms SMs (0 = all).
+la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
+                   int max_sms, cudaStream_t st, int *launches);
+
+la_status comm_destroy();
+
+}  // namespace la

@@ -1,0 +1,199 @@
+// multi.cu -- the multi-GPU partition.
+//
+// One process per GPU.  Rank r owns rows [r*n/g, (r+1)*n/g) of A and C.  B is
+// replicated with ncclBroadcast from `root` in N-panels (column blocks of B,
+// packed contiguously) on a library-owned communication stream; the caller's
+// stream waits for panel c, splits it and runs the GEMM on
+// A_r . B[:, panel c] while panels c+1.. are still in flight.  There is no K
+// split, so no reduction: C row blocks are complete where they are computed and
+// are optionally all-gathered (ncclAllGather) into the full n x p matrix.
+// Every output element accumulates in exactly the order la_gemm uses, so the
+// multi-GPU C is bitwise identical to the single-GPU C.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "la.h"
+#include "la_internal.h"
+
+namespace la {
+
+struct Comm {
+    ncclComm_t comm = nullptr;
+    int rank = -1, size = 0;
+    cudaStream_t stream = nullptr;  // communication stream
+    cudaEvent_t start = nullptr;
+    std::vector<cudaEvent_t> panel_ready;
+    void *bstage = nullptr;  // packed B panels (m x p floats), every rank
+    size_t bstage_bytes = 0;
+};
+static Comm g_comm;
+
+static la_status nccl_fail(ncclResult_t r, const char *what) {
+    return fail(LA_ERR_NCCL, "%s failed: %s", what, ncclGetErrorString(r));
+}
+
+#define LA_NCCL(call)                                      \
+    do {                                                   \
+        ncclResult_t r_ = (call);                          \
+        if (r_ != ncclSuccess) return nccl_fail(r_, #call); \
+    } while (0)
+#define LA_CK(call)                                                             \
+    do {                                                                        \
+        cudaError_t e_ = (call);                                                \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+la_status comm_destroy() {
+    la_status s = LA_OK;
+    if (g_comm.comm) {
+        ncclResult_t r = ncclCommDestroy(g_comm.comm);
+        if (r != ncclSuccess) s = nccl_fail(r, "ncclCommDestroy");
+    }
+    for (auto e : g_comm.panel_ready) cudaEventDestroy(e);
+    if (g_comm.start) cudaEventDestroy(g_comm.start);
+    if (g_comm.stream) cudaStreamDestroy(g_comm.stream);
+    if (g_comm.bstage) cudaFree(g_comm.bstage);
+    g_comm = Comm();
+    return s;
+}
+
+// SMs left free for NCCL's kernels while broadcasts are in flight.
+static int reserved_sms() {
+    if (const char *e = getenv("LA_NCCL_RESERVED_SMS")) return std::max(0, atoi(e));
+    return 8;
+}
+
+}  // namespace la
+
+using namespace la;
+
+extern "C" {
+
+la_status la_get_unique_id(void *out128) {
+    if (!out128) return fail(LA_ERR_INVALID_VALUE, "NULL unique-id buffer");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    LA_NCCL(ncclGetUniqueId(&id));
+    memcpy(out128, &id, sizeof id);
+    return LA_OK;
+}
+
+la_status la_comm_init(const void *uid128, int rank, int ngpu) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (!uid128 || ngpu < 1 || rank < 0 || rank >= ngpu)
+        return fail(LA_ERR_INVALID_VALUE, "bad communicator arguments rank=%d ngpu=%d", rank, ngpu);
+    if (g_comm.comm) {
+        la_status s = comm_destroy();
+        if (s != LA_OK) return s;
+    }
+    ncclUniqueId id;
+    memcpy(&id, uid128, sizeof id);
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 1;
+    LA_NCCL(ncclCommInitRankConfig(&g_comm.comm, ngpu, id, rank, &cfg));
+    g_comm.rank = rank;
+    g_comm.size = ngpu;
+    LA_CK(cudaStreamCreateWithFlags(&g_comm.stream, cudaStreamNonBlocking));
+    LA_CK(cudaEventCreateWithFlags(&g_comm.start, cudaEventDisableTiming));
+    return LA_OK;
+}
+
+la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local, const float *d_B,
+                        float *d_C_local, float *d_C_full, int root, int ngpu, void *stream) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (!g_comm.comm) return fail(LA_ERR_NOT_INITIALIZED, "la_comm_init has not been called");
+    if (ngpu != g_comm.size)
+        return fail(LA_ERR_INVALID_VALUE, "ngpu=%d but the communicator has %d ranks", ngpu, g_comm.size);
+    if (root < 0 || root >= ngpu) return fail(LA_ERR_INVALID_VALUE, "root %d out of range", root);
+    if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
+    if (n < ngpu) return fail(LA_ERR_UNSUPPORTED, "n=%lld < ngpu=%d leaves a rank without rows", (long long)n, ngpu);
+    if (d_C_full && n % ngpu != 0)
+        return fail(LA_ERR_UNSUPPORTED, "all-gather of C needs n %% ngpu == 0 (n=%lld, ngpu=%d)", (long long)n, ngpu);
+    const int rank = g_comm.rank;
+    if (rank == root && !d_B) return fail(LA_ERR_INVALID_VALUE, "B is NULL on the root rank");
+    if (!d_A_local || !d_C_local) return fail(LA_ERR_INVALID_VALUE, "NULL A_local or C_local");
+    int64_t row0 = 0, rows = 0;
+    la_shard_rows(n, rank, ngpu, &row0, &rows);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    // N-panels: widths are multiples of 128 (the GEMM's N tile) except the last.
+    int64_t P = std::max<int64_t>(1, g_state.panels);
+    int64_t pc = (p + P - 1) / P;
+    pc = (pc + 127) / 128 * 128;
+    P = (p + pc - 1) / pc;
+    while ((int64_t)g_comm.panel_ready.size() < P) {
+        cudaEvent_t e;
+        LA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        g_comm.panel_ready.push_back(e);
+    }
+    const size_t bbytes = (size_t)(m * p) * sizeof(float);
+    if (g_comm.bstage_bytes < bbytes) {
+        LA_CK(cudaDeviceSynchronize());
+        if (g_comm.bstage) LA_CK(cudaFree(g_comm.bstage));
+        g_comm.bstage = nullptr;
+        g_comm.bstage_bytes = 0;
+        cudaError_t e = cudaMalloc(&g_comm.bstage, bbytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(LA_ERR_OUT_OF_MEMORY, "B staging of %zu bytes", bbytes);
+        }
+        g_comm.bstage_bytes = bbytes;
+    }
+    float *bstage = static_cast<float *>(g_comm.bstage);
+
+    const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
+    const size_t wbytes = operands_bytes(rows, m, p, passes);
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&ws, wbytes, g_state.pool, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LA_ERR_OUT_OF_MEMORY, "workspace of %zu bytes", wbytes);
+    }
+    const Operands ops = operands_carve(ws, rows, m, p, passes);
+    int launches = 0;
+
+    // comm stream starts after everything already queued on the caller's stream
+    LA_CK(cudaEventRecord(g_comm.start, st));
+    LA_CK(cudaStreamWaitEvent(g_comm.stream, g_comm.start, 0));
+    for (int64_t c = 0; c < P; c++) {
+        const int64_t j0 = c * pc, w = std::min(pc, p - j0);
+        float *panel = bstage + m * j0;  // packed m x w panel
+        if (rank == root) {
+            if (P == 1) {
+                LA_NCCL(ncclBroadcast(d_B, panel, (size_t)(m * w), ncclFloat, root, g_comm.comm, g_comm.stream));
+            } else {
+                LA_CK(cudaMemcpy2DAsync(panel, w * sizeof(float), d_B + j0, p * sizeof(float), w * sizeof(float),
+                                        m, cudaMemcpyDeviceToDevice, g_comm.stream));
+                LA_NCCL(ncclBroadcast(panel, panel, (size_t)(m * w), ncclFloat, root, g_comm.comm, g_comm.stream));
+            }
+        } else {
+            LA_NCCL(ncclBroadcast(nullptr, panel, (size_t)(m * w), ncclFloat, root, g_comm.comm, g_comm.stream));
+        }
+        LA_CK(cudaEventRecord(g_comm.panel_ready[c], g_comm.stream));
+    }
+
+    la_status s = split_a(rows, m, d_A_local, ops, st, &launches);
+    const int reserve = ngpu > 1 ? reserved_sms() : 0;
+    for (int64_t c = 0; c < P && s == LA_OK; c++) {
+        const int64_t j0 = c * pc, w = std::min(pc, p - j0);
+        LA_CK(cudaStreamWaitEvent(st, g_comm.panel_ready[c], 0));
+        s = split_b(m, j0, w, bstage + m * j0, w, ops, st, &launches);
+        if (s != LA_OK) break;
+        const int max_sms = (c < P - 1 && reserve > 0) ? std::max(1, g_state.sms - reserve) : (int)g_state.max_sms;
+        s = gemm_run(rows, m, j0, w, ops, d_C_local, p, max_sms, st, &launches);
+    }
+    e = cudaFreeAsync(ws, st);
+    if (s != LA_OK) return s;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);
+    if (d_C_full)
+        LA_NCCL(ncclAllGather(d_C_local, d_C_full, (size_t)(rows * p), ncclFloat, g_comm.comm, st));
+    g_state.last_launches = launches;
+    return LA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// split.cuh -- K1: operand split for the 3xTF32 product (HBM-bound pass).
+//
+// a = hi + lo,  hi = tf32_rna(a) (11 significant bits, low 13 mantissa bits 0),
+// lo = a - hi   (exact in fp32: the rounding error of rounding to fewer bits).
+// The tensor pipe then forms hi*hi' + hi*lo' + lo*hi' (lo*lo' <= 2^-22 |a a'|
+// is dropped).  Not in the paper (its kernels multiply fp32 on SIMT cores,
+// P:118); it is how fp32 accuracy comes off the TF32 tensor pipe
+// (BASELINE.json north_star).
+//
+// Layouts written (the GEMM's TMA descriptors read them):
+//   A (n x m row-major)  -> A_hi, A_lo : n x mp row-major, mp = round_up(m, 4)
+//   B (m x p row-major)  -> Bt_hi, Bt_lo: p x mp row-major (B transposed, so both
+//                           operands are K-major for the UMMA descriptors)
+// Columns [m, mp) are written as 0 so TMA rows are 16-byte aligned and the
+// padding contributes exact zeros.  With PASSES == 1 (plain TF32 mode) only hi
+// is written.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace la {
+
+template <int PASSES>
+__device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64_t off) {
+    const float h = ptx::to_tf32_rna(x);
+    hi[off] = h;
+    if constexpr (PASSES == 3) lo[off] = x - h;
+}
+
+// Row-major A, m % 4 == 0: flat float4 grid-stride loop (mp == m).
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__restrict__ a,
+                                                              float4 *__restrict__ hi,
+                                                              float4 *__restrict__ lo,
+                                                              int64_t count4) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = __ldcs(a + i);
+        float4 h, l;
+        h.x = ptx::to_tf32_rna(x.x);
+        h.y = ptx::to_tf32_rna(x.y);
+        h.z = ptx::to_tf32_rna(x.z);
+        h.w = ptx::to_tf32_rna(x.w);
+        __stcg(hi + i, h);
+        if constexpr (PASSES == 3) {
+            l.x = x.x - h.x;
+            l.y = x.y - h.y;
+            l.z = x.z - h.z;
+            l.w = x.w - h.w;
+            __stcg(lo + i, l);
+        }
+    }
+}
+
+// Row-major A, general m: one block-row per grid.y step, columns padded to mp.
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_rows_kernel(const float *__restrict__ a,
+                                                         float *__restrict__ hi,
+                                                         float *__restrict__ lo, int64_t n,
+                                                         int64_t m, int64_t mp) {
+    for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
+        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < mp;
+             c += (int64_t)gridDim.x * blockDim.x) {
+            const float x = c < m ? a[r * m + c] : 0.0f;
+            split_store<PASSES>(x, hi, lo, r * mp + c);
+        }
+    }
+}
+
+// B (m x p block, row stride ldb) -> Bt (p x mp row-major), 32x32 tiles through
+// smem so both the read (along j) and the write (along k) are coalesced.
+// Block (32, 8).
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_transpose_kernel(const float *__restrict__ b,
+                                                              float *__restrict__ hi,
+                                                              float *__restrict__ lo, int64_t m,
+                                                              int64_t p, int64_t ldb, int64_t mp) {
+    __shared__ float tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t j0 = (int64_t)blockIdx.x * 32;  // column of B = row of Bt
+    const int64_t k0 = (int64_t)blockIdx.y * 32;  // row of B = column of Bt
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t k = k0 + ty + 8 * i, j = j0 + tx;
+        tile[ty + 8 * i][tx] = (k < m && j < p) ? __ldcs(b + k * ldb + j) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t j = j0 + ty + 8 * i, k = k0 + tx;
+        if (j < p && k < mp) split_store<PASSES>(tile[tx][ty + 8 * i], hi, lo, j * mp + k);
+    }
+}
+
+}  // namespace la

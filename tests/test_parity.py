@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * integer-valued inputs: value-exact (==) against the oracle;
+  * random inputs, 3xTF32: |C - C_ref| <= 2^-20 * sum_r |a_ir||b_rj| per element;
+  * random inputs, TF32:   |C - C_ref| <= 2^-9  * sum_r |a_ir||b_rj|;
+  * index mapping: identity and permutation products bit-exact (23-bit inputs
+    satisfy hi + lo == a exactly, and one nonzero product per element is exact).
+Sizes span several tiles and ragged tails; full-size configs are checked on
+sampled elements the oracle computes one by one, plus Freivalds over the whole
+of C for integer inputs.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+THREADS = max(1, len(os.sched_getaffinity(0)))
+TOL = {"3xtf32": 2.0 ** -20, "tf32": 2.0 ** -9}
+
+
+@pytest.fixture(scope="module")
+def la():
+    import paper_1306_6192_b200 as la
+    la.init(0)
+    la.set_mode("3xtf32")
+    yield la
+    la.set_mode("3xtf32")
+
+
+def _gpu(la, A, B, mode="3xtf32"):
+    la.set_mode(mode)
+    try:
+        C = la.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+        torch.cuda.synchronize()
+    finally:
+        la.set_mode("3xtf32")
+    return C.cpu().numpy()
+
+
+def _check(A, B, C, kind, mode):
+    Cref = oracle.gemm(A, B, threads=THREADS)
+    if kind == "integer":
+        bad = np.argwhere(C != Cref)
+        assert bad.size == 0, f"{len(bad)} elements differ, first {bad[:3].tolist()}"
+        return 0.0
+    S = oracle.abs_scale(A, B)
+    err = np.abs(C.astype(np.float64) - Cref.astype(np.float64))
+    ratio = err / np.maximum(S, np.finfo(np.float64).tiny)
+    worst = float(ratio.max())
+    assert worst <= TOL[mode], f"max |C-C_ref|/S = {worst:.3g} = {worst / TOL[mode]:.3f} x tol"
+    return worst
+
+
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("kind", ["integer", "random", "stress"])
+def test_config1_square_256(la, kind, mode):
+    A, B = [x.numpy() for x in inputs.pair(256, 256, 256, kind)]
+    _check(A, B, _gpu(la, A, B, mode), kind, mode)
+
+
+@pytest.mark.parametrize("kind", ["integer", "random", "stress"])
+def test_config2_rectangular_ragged(la, kind):
+    """1000x2000 . 2000x1500: M tail 1000 = 7*128+104, N tail 1500 = 11*128+92,
+    K tail 2000 = 62*32+16 (BASELINE.json configs[1])."""
+    A, B = [x.numpy() for x in inputs.pair(1000, 2000, 1500, kind)]
+    _check(A, B, _gpu(la, A, B), kind, "3xtf32")
+
+
+RAGGED = [1, 2, 7, 8, 15, 16, 17, 31, 32, 33, 127, 128, 129, 255, 256, 257]
+
+
+@pytest.mark.parametrize("n", [1, 17, 128, 129, 257])
+@pytest.mark.parametrize("m", [1, 3, 7, 31, 32, 33, 129, 1000])
+@pytest.mark.parametrize("p", [1, 2, 15, 128, 255, 257])
+def test_ragged_lattice_integer_exact(la, n, m, p):
+    A = inputs.generate(n, m, 0, "integer").numpy()
+    B = inputs.generate(m, p, 1, "integer").numpy()
+    _check(A, B, _gpu(la, A, B), "integer", "3xtf32")
+
+
+@pytest.mark.parametrize("n,m,p", [(129, 257, 255), (33, 1000, 511), (300, 64, 129), (2, 5000, 3)])
+def test_ragged_random_within_bound(la, n, m, p):
+    A, B = [x.numpy() for x in inputs.pair(n, m, p, "stress")]
+    _check(A, B, _gpu(la, A, B), "stress", "3xtf32")
+
+
+def test_identity_and_permutation_bit_exact(la):
+    rng = np.random.default_rng(1)
+    A = inputs.generate(300, 260, 0, "random").numpy()           # 23-bit significands
+    I = np.eye(260, dtype=np.float32)
+    assert np.array_equal(_gpu(la, A, I), A)
+    I2 = np.eye(300, dtype=np.float32)
+    assert np.array_equal(_gpu(la, I2, A), A)
+    pr, pc = rng.permutation(300), rng.permutation(260)
+    assert np.array_equal(_gpu(la, I2[pr], A), A[pr])
+    assert np.array_equal(_gpu(la, A, I[:, pc]), A[:, pc])
+
+
+def test_diagonal_and_transpose_within_bound(la):
+    rng = np.random.default_rng(2)
+    d = inputs.generate(1, 200, 0, "stress").numpy()[0]
+    B = inputs.generate(200, 150, 1, "stress").numpy()
+    D = np.diag(d).astype(np.float32)
+    _check(D, B, _gpu(la, D, B), "stress", "3xtf32")
+    A, B = [x.numpy() for x in inputs.pair(190, 333, 170, "stress")]
+    C = _gpu(la, A, B)
+    Ct = _gpu(la, np.ascontiguousarray(B.T), np.ascontiguousarray(A.T))
+    S = oracle.abs_scale(A, B)
+    assert np.all(np.abs(Ct.T.astype(np.float64) - C) <= 2 * 2.0 ** -20 * S)
+
+
+def test_run_to_run_bitwise(la):
+    A, B = inputs.pair(700, 900, 650, "random", device="cuda")
+    C1 = la.gemm(A, B)
+    C2 = la.gemm(A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)
+
+
+def test_launch_count_and_stream(la):
+    A, B = inputs.pair(256, 256, 256, "integer", device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        C = la.gemm(A, B, stream=s)
+    s.synchronize()
+    assert la.last_launch_count() == 3          # split A, split B, GEMM
+    ref = (A.cpu().double() @ B.cpu().double()).float()
+    assert torch.equal(C.cpu(), ref)
+
+
+def test_graph_capture(la):
+    A, B = inputs.pair(512, 384, 640, "integer", device="cuda")
+    C = torch.empty(512, 640, device="cuda")
+    la.gemm(A, B, out=C)
+    torch.cuda.synchronize()
+    ref = C.clone()
+    C.zero_()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=s):
+        la.gemm(A, B, out=C, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
+
+
+def test_host_entry_point(la):
+    A, B = [x.numpy() for x in inputs.pair(333, 444, 555, "integer")]
+    C = la.gemm_host(A, B)
+    assert np.array_equal(C, oracle.gemm(A, B, threads=THREADS))
+    Ap, Bp = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+    Cp = torch.empty(333, 555).pin_memory()
+    la.gemm_host(Ap, Bp, out=Cp)
+    assert np.array_equal(Cp.numpy(), C)
+
+
+def test_error_paths_on_gpu(la):
+    A = torch.zeros(4, 4, device="cuda")
+    lib = la._lib
+    assert lib.la_gemm(0, 4, 4, A.data_ptr(), A.data_ptr(), A.data_ptr() + 64, None) == la.LA_ERR_INVALID_VALUE
+    assert lib.la_gemm(4, 4, 4, 0, A.data_ptr(), A.data_ptr(), None) == la.LA_ERR_INVALID_VALUE
+    # C aliasing A
+    assert lib.la_gemm(4, 4, 4, A.data_ptr(), A.data_ptr(), A.data_ptr(), None) == la.LA_ERR_INVALID_VALUE
+    assert lib.la_init(0) == la.LA_OK                       # idempotent
+
+
+# --------------------------------------------------------------------------- #
+# Full-size configurations, checked on sampled elements (oracle one by one on
+# the sampled rows x columns, inputs regenerated on the host) and, for integer
+# inputs, Freivalds over all of C.
+# --------------------------------------------------------------------------- #
+def _sample_idx(n, tile, rng, k=48):
+    idx = set(rng.choice(n, size=min(k, n), replace=False).tolist())
+    for b in range(0, n, tile * 16):
+        idx.update(x for x in (b - 1, b, b + 1) if 0 <= x < n)
+    idx.update([0, n - 1])
+    return sorted(idx)
+
+
+def _sampled_check(la, n, m, p, kind, mode="3xtf32", freivalds=False):
+    A, B = inputs.pair(n, m, p, kind, device="cuda")
+    la.set_mode(mode)
+    try:
+        C = la.gemm(A, B)
+    finally:
+        la.set_mode("3xtf32")
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(n + m + p)
+    rows, cols = _sample_idx(n, 128, rng), _sample_idx(p, 128, rng)
+    As = inputs.generate(n, m, 0, kind, row_idx=rows).numpy()
+    Bs = inputs.generate(m, p, 1, kind, col_idx=cols).numpy()
+    Cs = C[rows][:, cols].cpu().numpy()
+    worst = _check(As, Bs, Cs, kind, mode)
+    if freivalds:
+        x = np.random.default_rng(7).integers(-8, 9, size=p)
+        bad = oracle.freivalds(A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy(), x)
+        assert bad == 0, f"Freivalds: {bad} rows of C are wrong"
+    return worst
+
+
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_config3_4096_sampled(la, mode):
+    _sampled_check(la, 4096, 4096, 4096, "random", mode)
+
+
+def test_config3_4096_integer_freivalds(la):
+    _sampled_check(la, 4096, 4096, 4096, "integer", freivalds=True)
+
+
+@pytest.mark.parametrize("kind", ["random", "stress"])
+def test_config4_16384_sampled(la, kind):
+    _sampled_check(la, 16384, 16384, 16384, kind)
+
+
+def test_config4_16384_integer_freivalds(la):
+    _sampled_check(la, 16384, 16384, 16384, "integer", freivalds=True)
