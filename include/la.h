@@ -77,7 +77,11 @@ typedef enum {
      * multi-GPU path uses it to leave SMs for NCCL. */
     LA_OPT_MAX_SMS = 1,
     /* Number of N-panels B is broadcast in by la_gemm_multi (>= 1). */
-    LA_OPT_PANELS = 2
+    LA_OPT_PANELS = 2,
+    /* 1: record CUDA events around every split and GEMM launch so that
+     * la_kernel_times() can report their device durations (bench.py's
+     * roofline).  0 (default): no events. */
+    LA_OPT_KERNEL_TIMING = 3
 } la_option;
 
 /* Bind the calling thread's library state to CUDA device `device`, check that it
@@ -154,6 +158,13 @@ LA_API const char *la_last_error(void);
 
 /* Number of kernels the last la_gemm / la_gemm_multi call launched. */
 LA_API int la_last_launch_count(void);
+
+/* With LA_OPT_KERNEL_TIMING = 1: synchronise on the recorded events and return
+ * the summed device time (ms) of the split kernels and of the GEMM kernels of
+ * every call since the previous la_kernel_times(), and how many GEMM launches
+ * that covers; then forget them.  Events are recorded on the caller's stream,
+ * the stream the kernels run on.  Errors: INVALID_VALUE (NULL), CUDA. */
+LA_API la_status la_kernel_times(double *split_ms, double *gemm_ms, int *gemm_launches);
 
 #ifdef __cplusplus
 }

@@ -23,12 +23,12 @@ LIB_PATH = os.path.join(_PKG, "libla.so")
 LA_OK, LA_ERR_INVALID_VALUE, LA_ERR_NOT_INITIALIZED, LA_ERR_UNSUPPORTED, \
     LA_ERR_OUT_OF_MEMORY, LA_ERR_CUDA, LA_ERR_NCCL = range(7)
 MODES = {"3xtf32": 0, "tf32": 1}
-OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2}
+OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3}
 
 # every symbol include/la.h declares (checked by tests/test_abi.py)
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
-           "la_status_string", "la_last_error", "la_last_launch_count")
+           "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times")
 
 
 class LaError(RuntimeError):
@@ -57,6 +57,8 @@ def _load() -> ctypes.CDLL:
         "la_status_string": ([ctypes.c_int], ctypes.c_char_p),
         "la_last_error": ([], ctypes.c_char_p),
         "la_last_launch_count": ([], ctypes.c_int),
+        "la_kernel_times": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(ctypes.c_int)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -107,6 +109,14 @@ def get_option(name: str) -> int:
 
 def last_launch_count() -> int:
     return _lib.la_last_launch_count()
+
+
+def kernel_times():
+    """(split_ms, gemm_ms, gemm_launches) summed over calls since the last query
+    (needs set_option('kernel_timing', 1))."""
+    a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    _check(_lib.la_kernel_times(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "la_kernel_times")
+    return a.value, b.value, c.value
 
 
 def _stream_ptr(stream):

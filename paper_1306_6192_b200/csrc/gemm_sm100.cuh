@@ -5,21 +5,32 @@
 // (P:178), does 16 FMAs per thread, synchronises again and
 // writes one C element per thread.  The same structure, re-built
 // for sm_100a:
-//   * staging     : TMA (cp.async.bulk.tensor) fills a STAGES-deep ring of
-//                   128B-swizzled K-major tiles; mbarrier full[s] replaces the
-//                   first __syncthreads;
+//   * staging      : TMA (cp.async.bulk.tensor) fills a STAGES-deep ring of
+//                    128B-swizzled K-major tiles; mbarrier full[s] replaces the
+//                    first __syncthreads;
 //   * inner product: one elected thread issues tcgen05.mma.kind::tf32 into a
-//                   TMEM accumulator (3 passes hi.lo', lo.hi', hi.hi' per K=8
-//                   step for 3xTF32); tcgen05.commit -> empty[s] replaces the
-//                   second __syncthreads;
-//   * write-back  : epilogue warps tcgen05.ld the accumulator, optionally add it
-//                   into an fp32 register running sum every `kc` K-blocks
-//                   (accumulator promotion), and store C exactly once per
-//                   element, coalesced through a per-warp smem transpose, with
-//                   64-bit offsets and ragged-edge predication.
-// Two TMEM accumulator buffers let the epilogue of one tile (or chunk) overlap
-// the MMAs of the next.  One CTA per SM, persistent over output tiles in a
-// grouped raster order (tiles sharing A rows run concurrently -> L2 reuse).
+//                    TMEM accumulator (3 passes hi.lo', lo.hi', hi.hi' per K=8
+//                    step for 3xTF32); tcgen05.commit -> empty[s] replaces the
+//                    second __syncthreads;
+//   * write-back   : epilogue warps tcgen05.ld the accumulator and store C
+//                    exactly once per element, coalesced through a
+//                    per-warp smem transpose, 64-bit offsets, ragged edges
+//                    predicated.
+// Accumulator promotion: the tcgen05 tf32 path sums each K=8 group exactly and
+// then TRUNCATES into the fp32 accumulator (measured, tests/test_probe.py), a
+// bias that grows with the number of MMAs per accumulator (3.1 x 2^-20 S at
+// K=16384).  So the MMA warp accumulates `kc` K-blocks per TMEM chunk and the
+// epilogue adds every chunk into an fp32 round-to-nearest register running
+// sum (0.06 x 2^-20 S at kc = 8 blocks of 32).  Two TMEM accumulator buffers
+// let the epilogue of chunk c overlap the MMAs of chunk c+1.
+//
+// CG == 1: one CTA computes a 128 x BN tile (UMMA M=128).
+// CG == 2: a cluster of two CTAs (a CTA pair on one TPC) computes a 256 x BN
+//          tile with tcgen05.mma.cta_group::2 (UMMA M=256): each CTA stages its
+//          128 rows of A and BN/2 rows of B^T, the leader CTA issues the MMAs,
+//          and each CTA's TMEM holds its 128 rows of the accumulator.  Operand
+//          traffic per FLOP is half that of CG == 1 at the same BN.
+// Persistent: one CTA (pair) per SM (pair), tiles in grouped raster order.
 #pragma once
 #include <cstdint>
 
@@ -27,10 +38,21 @@
 
 namespace la {
 
-constexpr int BM = 128;  // rows of C per CTA (UMMA M, cta_group::1)
-constexpr int BK = 32;   // K per stage: 32 fp32 = one 128-byte swizzle row
-constexpr int EPI_WARP0 = 4;
-constexpr int NUM_THREADS = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 idle, warps4-7 epilogue
+constexpr int BK = 32;            // K per stage: 32 fp32 = one 128-byte swizzle row
+constexpr int ROWS_PER_CTA = 128; // UMMA M per CTA
+constexpr int NUM_CTRL_WARPS = 4; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 idle
+constexpr int NUM_EPI_WARPS = 8;  // two per TMEM lane quarter (column halves)
+constexpr int NUM_THREADS = 32 * (NUM_CTRL_WARPS + NUM_EPI_WARPS);
+// setmaxnreg budgets.  A CTA's register pool is what it was launched with:
+// __launch_bounds__(384, 1) gives 168 registers x 384 threads = 64512; the
+// control warpgroup shrinks to CTRL_REGS and the two epilogue warpgroups grow
+// to EPI_REGS, and the sum must stay inside that pool or setmaxnreg.inc
+// blocks forever.
+constexpr int LAUNCH_REGS = 168;
+constexpr int CTRL_REGS = 56;
+constexpr int EPI_REGS = 216;
+static_assert(32 * NUM_CTRL_WARPS * CTRL_REGS + 32 * NUM_EPI_WARPS * EPI_REGS <= NUM_THREADS * LAUNCH_REGS,
+              "setmaxnreg budget exceeds the CTA's register pool");
 
 struct GemmArgs {
     float *C;
@@ -40,23 +62,27 @@ struct GemmArgs {
     int32_t tiles_m, tiles_n, group_m;
 };
 
-template <int BN, int STAGES, int PASSES>
+template <int CG, int BN, int STAGES, int PASSES>
 struct GemmCfg {
-    static constexpr int NOPS = PASSES == 3 ? 2 : 1;  // hi (+ lo) tiles per operand
-    static constexpr int A_TILE = BM * BK * 4;        // 16 KB
-    static constexpr int B_TILE = BN * BK * 4;
-    static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);
-    static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // per-warp 32x33 transpose buffers
+    static constexpr int TILE_M = CG * ROWS_PER_CTA;        // rows of C per tile
+    static constexpr int B_ROWS = BN / CG;                  // rows of B^T staged per CTA
+    static constexpr int NOPS = PASSES == 3 ? 2 : 1;        // hi (+ lo) tiles per operand
+    static constexpr int A_TILE = ROWS_PER_CTA * BK * 4;    // 16 KB
+    static constexpr int B_TILE = B_ROWS * BK * 4;
+    static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);  // per CTA
+    static constexpr int EPI_BYTES = NUM_EPI_WARPS * 32 * 32 * 4; // per-warp transpose buffers
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
-    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "UMMA N for M=128 must be a multiple of 16 <= 256");
-    static_assert(TMEM_COLS == 64 || TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM alloc");
+    static constexpr int COLS_PER_WARP = BN / 2;   // epilogue column half
+    static constexpr int PIECES = COLS_PER_WARP / 32;
+    static_assert(CG == 1 || CG == 2, "cta_group");
+    static_assert(BN % 64 == 0 && BN <= 256, "UMMA N: multiple of 16 (32 per epilogue piece), <= 256");
+    static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM alloc is a power of 2");
     static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int &tm,
-                                            int &tn) {
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int &tm, int &tn) {
     const int per_group = group * tiles_n;
     const int g = t / per_group;
     const int first = g * group;
@@ -67,36 +93,37 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 }
 
 // Write one 32 x 32 piece of C held as (thread = row, v[i] = column i) through
-// a per-warp padded smem transpose, so each store instruction writes 128
-// contiguous bytes of one C row.  Rows >= n and columns >= p are skipped
-// (ragged edges); offsets are 64-bit.
+// a per-warp XOR-swizzled smem transpose (conflict-free both ways), so each
+// store instruction writes 128 contiguous bytes of one C row.  Rows >= n and
+// columns >= p are skipped (ragged edges); offsets are 64-bit.
 __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, uint32_t lane, int64_t row0,
                                             int64_t col0, const uint32_t (&v)[32]) {
 #pragma unroll
-    for (int i = 0; i < 32; i++) tbuf[lane * 33 + i] = __uint_as_float(v[i]);
+    for (int i = 0; i < 32; i++) tbuf[lane * 32 + (i ^ lane)] = __uint_as_float(v[i]);
     __syncwarp();
     const int64_t col = col0 + lane;
-    if (col < args.p) {
+    const int64_t rem = args.n - row0;
+    if (col < args.p && rem > 0) {
         float *cp = args.C + row0 * args.ldc + col;
-        const int64_t rem = args.n - row0;
-        const int rows = rem < 32 ? (int)rem : 32;
-#pragma unroll 8
-        for (int rr = 0; rr < 32; rr++)
-            if (rr < rows) cp[rr * args.ldc] = tbuf[rr * 33 + lane];
+        if (rem >= 32) {
+#pragma unroll 4
+            for (int rr = 0; rr < 32; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
+        } else {
+            for (int rr = 0; rr < (int)rem; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
+        }
     }
     __syncwarp();
 }
 
-template <int BN, int STAGES, int PASSES>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_tf32_sm100_kernel(const __grid_constant__ CUtensorMap tm_a_hi,
-                           const __grid_constant__ CUtensorMap tm_a_lo,
-                           const __grid_constant__ CUtensorMap tm_b_hi,
-                           const __grid_constant__ CUtensorMap tm_b_lo, const GemmArgs args) {
-    using Cfg = GemmCfg<BN, STAGES, PASSES>;
+template <int CG, int BN, int STAGES, int PASSES>
+__global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tf32_sm100_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
+                           const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
+                           const GemmArgs args) {
+    using Cfg = GemmCfg<CG, BN, STAGES, PASSES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // stage s: [A_hi | A_lo | B_hi | B_lo]
+    // stage s: [A_hi | A_lo | B_hi | B_lo]   (identical offsets in both CTAs of a pair)
     auto a_tile = [&](int s, int op) { return smem + s * Cfg::STAGE_BYTES + op * Cfg::A_TILE; };
     auto b_tile = [&](int s, int op) {
         return smem + s * Cfg::STAGE_BYTES + Cfg::NOPS * Cfg::A_TILE + op * Cfg::B_TILE;
@@ -110,6 +137,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;  // CTA rank in the pair
+    const int cluster_id = blockIdx.x / CG;
+    const int num_clusters = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_a_hi);
@@ -121,18 +151,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < STAGES; s++) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&full[s], 1);   // leader producer's arrive.expect_tx (+ tx bytes of both CTAs)
+            ptx::mbar_init(&empty[s], 1);  // one tcgen05.commit (multicast to both CTAs)
         }
         for (int b = 0; b < 2; b++) {
-            ptx::mbar_init(&tfull[b], 1);
-            ptx::mbar_init(&tempty[b], 128);
+            ptx::mbar_init(&tfull[b], 1);                      // one tcgen05.commit
+            ptx::mbar_init(&tempty[b], CG * NUM_EPI_WARPS);    // one arrive per epilogue warp of the pair
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 2) ptx::tmem_alloc<1>(tmem_holder, Cfg::TMEM_COLS);
+    if (warp == 2) ptx::tmem_alloc<CG>(tmem_holder, Cfg::TMEM_COLS);
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
@@ -140,42 +170,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int num_kb = args.num_kb;
     const int kc = args.kc;
 
+    // Register budget per warpgroup role (setmaxnreg must dominate the role's
+    // code, so it is the first statement of each warpgroup branch).
+    if (warp < NUM_CTRL_WARPS) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CTRL_REGS));
     if (warp == 0) {
-        // ======================= TMA producer =======================
+        // ======================= TMA producer (both CTAs) =======================
         const uint64_t pol = ptx::policy_evict_normal();
         int s = 0;
         uint32_t ph = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
             int tm, tn;
             tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
-            const int32_t m0 = tm * BM, n0 = tn * BN;
+            const int32_t m0 = tm * Cfg::TILE_M + rank * ROWS_PER_CTA;
+            const int32_t n0 = tn * BN + rank * Cfg::B_ROWS;
             for (int kb = 0; kb < num_kb; kb++) {
                 ptx::mbar_wait(&empty[s], ph ^ 1);
                 if (lane == 0) {
                     const int32_t k0 = kb * BK;
-                    ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                    ptx::tma_load_2d(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
-                    ptx::tma_load_2d(b_tile(s, 0), &tm_b_hi, &full[s], k0, n0, pol);
-                    if constexpr (PASSES == 3) {
-                        ptx::tma_load_2d(a_tile(s, 1), &tm_a_lo, &full[s], k0, m0, pol);
-                        ptx::tma_load_2d(b_tile(s, 1), &tm_b_lo, &full[s], k0, n0, pol);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], CG * Cfg::STAGE_BYTES);
+                    if constexpr (CG == 1) {
+                        ptx::tma_load_2d(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
+                        ptx::tma_load_2d(b_tile(s, 0), &tm_b_hi, &full[s], k0, n0, pol);
+                        if constexpr (PASSES == 3) {
+                            ptx::tma_load_2d(a_tile(s, 1), &tm_a_lo, &full[s], k0, m0, pol);
+                            ptx::tma_load_2d(b_tile(s, 1), &tm_b_lo, &full[s], k0, n0, pol);
+                        }
+                    } else {
+                        ptx::tma_load_2d_pair(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
+                        ptx::tma_load_2d_pair(b_tile(s, 0), &tm_b_hi, &full[s], k0, n0, pol);
+                        if constexpr (PASSES == 3) {
+                            ptx::tma_load_2d_pair(a_tile(s, 1), &tm_a_lo, &full[s], k0, m0, pol);
+                            ptx::tma_load_2d_pair(b_tile(s, 1), &tm_b_lo, &full[s], k0, n0, pol);
+                        }
                     }
                 }
                 __syncwarp();
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
-    } else if (warp == 1) {
-        // ======================= MMA issuer =======================
-        constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN);
+    } else if (warp == 1 && rank == 0) {
+        // ======================= MMA issuer (leader CTA) =======================
+        constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::TILE_M, BN);
         int s = 0;
         uint32_t ph = 0, buf = 0, aph = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
             for (int kb = 0; kb < num_kb; kb++) {
-                const bool chunk_first = (kb % kc) == 0;
-                const bool chunk_last = (kb % kc) == kc - 1 || kb == num_kb - 1;
+                const int kin = kb % kc;
+                const bool chunk_first = kin == 0;
+                const bool chunk_last = kin == kc - 1 || kb == num_kb - 1;
                 if (chunk_first) {
-                    ptx::mbar_wait(&tempty[buf], aph ^ 1);
+                    if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[buf], aph ^ 1);
+                    else ptx::mbar_wait(&tempty[buf], aph ^ 1);
                     ptx::tc_fence_after();
                 }
                 ptx::mbar_wait(&full[s], ph);
@@ -186,22 +232,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t al = ptx::smem_u32(a_tile(s, PASSES == 3 ? 1 : 0));
                     const uint32_t bl = ptx::smem_u32(b_tile(s, PASSES == 3 ? 1 : 0));
 #pragma unroll
-                    for (int j = 0; j < BK / 8; j++) {  // K = 8 per tf32 MMA = 32 bytes
+                    for (int j = 0; j < BK / 8; j++) {  // K = 8 per tf32 MMA = 32 bytes of a swizzled row
                         const uint64_t dah = ptx::sdesc_kmajor_sw128(ah + 32 * j);
                         const uint64_t dbh = ptx::sdesc_kmajor_sw128(bh + 32 * j);
                         const uint32_t acc = (chunk_first && j == 0) ? 0u : 1u;
                         if constexpr (PASSES == 3) {
                             const uint64_t dal = ptx::sdesc_kmajor_sw128(al + 32 * j);
                             const uint64_t dbl = ptx::sdesc_kmajor_sw128(bl + 32 * j);
-                            ptx::mma_tf32<1>(d, dah, dbl, idesc, acc);  // hi . lo'
-                            ptx::mma_tf32<1>(d, dal, dbh, idesc, 1u);   // lo . hi'
-                            ptx::mma_tf32<1>(d, dah, dbh, idesc, 1u);   // hi . hi'
+                            ptx::mma_tf32<CG>(d, dah, dbl, idesc, acc);  // hi . lo'
+                            ptx::mma_tf32<CG>(d, dal, dbh, idesc, 1u);   // lo . hi'
+                            ptx::mma_tf32<CG>(d, dah, dbh, idesc, 1u);   // hi . hi'
                         } else {
-                            ptx::mma_tf32<1>(d, dah, dbh, idesc, acc);
+                            ptx::mma_tf32<CG>(d, dah, dbh, idesc, acc);
                         }
                     }
-                    ptx::mma_commit<1>(&empty[s]);
-                    if (chunk_last) ptx::mma_commit<1>(&tfull[buf]);
+                    ptx::mma_commit<CG>(&empty[s]);
+                    if (chunk_last) ptx::mma_commit<CG>(&tfull[buf]);
                 }
                 __syncwarp();
                 if (chunk_last) {
@@ -211,81 +257,82 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
-    } else if (warp >= EPI_WARP0) {
-        // ======================= epilogue =======================
-        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
-        float *tbuf = epi + (warp - EPI_WARP0) * (32 * 33);
-        const uint32_t lane_off = (32u * q) << 16;
+    }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
+        // ======================= epilogue (both CTAs) =======================
+        const uint32_t e = warp - NUM_CTRL_WARPS;
+        const uint32_t q = warp & 3;        // TMEM lane quarter this warp may access
+        const uint32_t half = e >> 2;       // column half of the accumulator
+        float *tbuf = epi + e * (32 * 32);
+        const uint32_t tq = tmem_base + ((32u * q) << 16) + half * Cfg::COLS_PER_WARP;
         uint32_t buf = 0, aph = 0;
         const int nchunks = (num_kb + kc - 1) / kc;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
             int tm, tn;
             tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
-            const int64_t row0 = (int64_t)tm * BM + 32 * q;
+            const int64_t row0 = (int64_t)tm * Cfg::TILE_M + rank * ROWS_PER_CTA + 32 * q;
+            const int64_t col0 = (int64_t)tn * BN + half * Cfg::COLS_PER_WARP;
             if (nchunks == 1) {
                 // whole K accumulated in TMEM: stream 32-column pieces to C
                 ptx::mbar_wait(&tfull[buf], aph);
                 ptx::tc_fence_after();
 #pragma unroll 1
-                for (int qq = 0; qq < BN / 32; qq++) {
+                for (int qq = 0; qq < Cfg::PIECES; qq++) {
                     uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(tmem_base + lane_off + buf * BN + qq * 32, v);
+                    ptx::tmem_ld_32x32b_x32(tq + buf * BN + qq * 32, v);
                     ptx::tmem_ld_wait();
-                    if (qq == BN / 32 - 1) {  // accumulator buffer free for the next tile
+                    if (qq == Cfg::PIECES - 1) {  // accumulator buffer free for the next tile
                         ptx::tc_fence_before();
-                        ptx::mbar_arrive(&tempty[buf]);
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     }
-                    store_piece(args, tbuf, lane, row0, (int64_t)tn * BN + qq * 32, v);
+                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v);
                 }
                 buf ^= 1;
                 if (buf == 0) aph ^= 1;
             } else {
                 // accumulator promotion: fp32 (RN) running sum of TMEM chunks
-                float acc[BN / 32][32];
+                float acc[Cfg::PIECES][32];
 #pragma unroll 1
                 for (int c = 0; c < nchunks; c++) {
                     ptx::mbar_wait(&tfull[buf], aph);
                     ptx::tc_fence_after();
-                    const uint32_t taddr = tmem_base + lane_off + buf * BN;
-                    if (c == 0) {
+                    const uint32_t taddr = tq + buf * BN;
 #pragma unroll
-                        for (int qq = 0; qq < BN / 32; qq++) {
-                            uint32_t v[32];
-                            ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v);
-                            ptx::tmem_ld_wait();
+                    for (int qq = 0; qq < Cfg::PIECES; qq++) {
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v);
+                        ptx::tmem_ld_wait();
+                        if (c == 0) {
 #pragma unroll
                             for (int i = 0; i < 32; i++) acc[qq][i] = __uint_as_float(v[i]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int qq = 0; qq < BN / 32; qq++) {
-                            uint32_t v[32];
-                            ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v);
-                            ptx::tmem_ld_wait();
+                        } else {
 #pragma unroll
                             for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v[i]);
                         }
                     }
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(&tempty[buf]);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     buf ^= 1;
                     if (buf == 0) aph ^= 1;
                 }
 #pragma unroll
-                for (int qq = 0; qq < BN / 32; qq++) {
+                for (int qq = 0; qq < Cfg::PIECES; qq++) {
                     uint32_t v[32];
 #pragma unroll
                     for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
-                    store_piece(args, tbuf, lane, row0, (int64_t)tn * BN + qq * 32, v);
+                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v);
                 }
             }
         }
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 2) ptx::tmem_dealloc<1>(tmem_base, Cfg::TMEM_COLS);
+    if (warp == 2) ptx::tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
 }
 
 }  // namespace la

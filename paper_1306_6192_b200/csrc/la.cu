@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "gemm_sm100.cuh"
 #include "la.h"
@@ -45,7 +46,6 @@ la_status cuda_fail(cudaError_t e, const char *what, const char *file, int line)
 }
 
 // Tuned kernel configurations.
-constexpr int kBN = 128;
 constexpr int kStages3 = 3;  // 3 x 64 KB stages for 3xTF32
 constexpr int kStages1 = 6;  // 6 x 32 KB stages for plain TF32
 
@@ -69,7 +69,7 @@ static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int
     if (!enc) return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};  // box_rows <= 256
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides,
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -77,6 +77,43 @@ static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int
     if (r != CUDA_SUCCESS)
         return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld", (int)r,
                     (long long)rows, (long long)cols);
+    return LA_OK;
+}
+
+// ---- optional per-kernel device timing (bench.py roofline) ----------------
+struct TimedSpan {
+    cudaEvent_t a, b;
+    TimedKind kind;
+};
+static std::vector<TimedSpan> g_spans;     // recorded, not yet read
+static std::vector<cudaEvent_t> g_free_ev;  // reusable events
+
+static cudaEvent_t take_event() {
+    if (!g_free_ev.empty()) {
+        cudaEvent_t e = g_free_ev.back();
+        g_free_ev.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+la_status timing_begin(cudaStream_t st, cudaEvent_t *ev) {
+    *ev = nullptr;
+    if (!g_state.kernel_timing) return LA_OK;
+    *ev = take_event();
+    cudaError_t e = cudaEventRecord(*ev, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord", __FILE__, __LINE__);
+    return LA_OK;
+}
+
+la_status timing_end(cudaStream_t st, cudaEvent_t ev, TimedKind kind) {
+    if (!ev) return LA_OK;
+    cudaEvent_t b = take_event();
+    cudaError_t e = cudaEventRecord(b, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord", __FILE__, __LINE__);
+    g_spans.push_back({ev, b, kind});
     return LA_OK;
 }
 
@@ -99,6 +136,9 @@ Operands operands_carve(void *ws, int64_t n, int64_t m, int64_t p, int passes) {
 }
 
 la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cudaStream_t st, int *launches) {
+    cudaEvent_t t0;
+    la_status ts = timing_begin(st, &t0);
+    if (ts != LA_OK) return ts;
     if (m % 4 == 0) {
         const int64_t count4 = n * m / 4;
         const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, (int64_t)g_state.sms * 8));
@@ -120,7 +160,7 @@ la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cud
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "split_a launch", __FILE__, __LINE__);
-    return LA_OK;
+    return timing_end(st, t0, TIMED_SPLIT);
 }
 
 la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb, const Operands &ops,
@@ -128,6 +168,9 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     dim3 grid((unsigned)((pc + 31) / 32), (unsigned)((ops.mp + 31) / 32));
     if (grid.y > 65535) return fail(LA_ERR_UNSUPPORTED, "m = %lld too large for the split grid", (long long)m);
     const float *b = B;  // B points at column j0 of the source matrix
+    cudaEvent_t t0;
+    la_status ts = timing_begin(st, &t0);
+    if (ts != LA_OK) return ts;
     float *hi = ops.b_hi + j0 * ops.mp, *lo = ops.b_lo + j0 * ops.mp;
     if (ops.passes == 3)
         split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
@@ -136,21 +179,21 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "split_b launch", __FILE__, __LINE__);
-    return LA_OK;
+    return timing_end(st, t0, TIMED_SPLIT);
 }
 
-template <int BN, int STAGES, int PASSES>
+template <int CG, int BN, int STAGES, int PASSES>
 static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C,
                              int64_t ldc, int max_sms, cudaStream_t st, int *launches) {
-    using Cfg = GemmCfg<BN, STAGES, PASSES>;
+    using Cfg = GemmCfg<CG, BN, STAGES, PASSES>;
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     la_status s;
     const float *bh = ops.b_hi + j0 * ops.mp, *bl = ops.b_lo + j0 * ops.mp;
-    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, BM)) != LA_OK) return s;
-    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, BN)) != LA_OK) return s;
+    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA)) != LA_OK) return s;
+    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS)) != LA_OK) return s;
     if (PASSES == 3) {
-        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, BM)) != LA_OK) return s;
-        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, BN)) != LA_OK) return s;
+        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, ROWS_PER_CTA)) != LA_OK) return s;
+        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, Cfg::B_ROWS)) != LA_OK) return s;
     } else {
         ta_lo = ta_hi;
         tb_lo = tb_hi;
@@ -164,32 +207,68 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     const int64_t pk = g_state.promote_k;
     args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + BK - 1) / BK);
     if (args.kc > args.num_kb) args.kc = args.num_kb;
-    args.tiles_m = (int32_t)((n + BM - 1) / BM);
+    args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
     args.group_m = 16;
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
-    int sms = g_state.sms;
-    if (max_sms > 0) sms = std::min(sms, max_sms);
-    const int grid = (int)std::min<int64_t>(tiles, sms);
 
-    auto kern = gemm_tf32_sm100_kernel<BN, STAGES, PASSES>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES>;
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)", __FILE__, __LINE__);
-        attr_set = true;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(CG * g_state.sms / CG);
+        cfg.blockDim = dim3(NUM_THREADS);
+        cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = CG;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+        if (e != cudaSuccess || nc <= 0) {
+            cudaGetLastError();
+            nc = g_state.sms / CG;
+        }
+        max_clusters = nc;
     }
-    kern<<<grid, NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, args);
+    int clusters = max_clusters;
+    if (max_sms > 0) clusters = std::min(clusters, std::max(1, max_sms / CG));
+    clusters = (int)std::min<int64_t>(tiles, clusters);
+    cudaEvent_t t0;
+    if ((s = timing_begin(st, &t0)) != LA_OK) return s;
+    kern<<<clusters * CG, NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, args);
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
-    return LA_OK;
+    return timing_end(st, t0, TIMED_GEMM);
+}
+
+// Kernel choice: the CTA-pair 256 x 256 kernel (half the operand traffic per
+// FLOP) once it fills at least one wave of SM pairs, else the single-CTA
+// 128 x 128 kernel, which spreads small or thin problems over 4x more tiles.
+static int choose_cta_group(int64_t n, int64_t pc) {
+    if (const char *e = getenv("LA_CTA_GROUP")) {
+        const int v = atoi(e);
+        if (v == 1 || v == 2) return v;
+    }
+    const int64_t pair_tiles = ((n + 255) / 256) * ((pc + 255) / 256);
+    return pair_tiles >= g_state.sms / 2 ? 2 : 1;
 }
 
 la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
                    int max_sms, cudaStream_t st, int *launches) {
-    if (ops.passes == 3) return launch_gemm<kBN, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
-    return launch_gemm<kBN, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+    const int cg = choose_cta_group(n, pc);
+    if (ops.passes == 3) {
+        if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+        return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+    }
+    if (cg == 2) return launch_gemm<2, 256, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+    return launch_gemm<1, 128, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
 }
 
 la_status validate_gemm(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const float *C) {
@@ -298,6 +377,10 @@ la_status la_set_option(la_option option, int64_t value) {
             if (value < 1) return fail(LA_ERR_INVALID_VALUE, "panels must be >= 1");
             g_state.panels = value;
             return LA_OK;
+        case LA_OPT_KERNEL_TIMING:
+            if (value != 0 && value != 1) return fail(LA_ERR_INVALID_VALUE, "kernel_timing is 0 or 1");
+            g_state.kernel_timing = value == 1;
+            return LA_OK;
     }
     return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
 }
@@ -308,6 +391,7 @@ la_status la_get_option(la_option option, int64_t *value) {
         case LA_OPT_PROMOTE_K: *value = g_state.promote_k; return LA_OK;
         case LA_OPT_MAX_SMS: *value = g_state.max_sms; return LA_OK;
         case LA_OPT_PANELS: *value = g_state.panels; return LA_OK;
+        case LA_OPT_KERNEL_TIMING: *value = g_state.kernel_timing ? 1 : 0; return LA_OK;
     }
     return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
 }
@@ -399,5 +483,27 @@ const char *la_status_string(la_status s) {
 const char *la_last_error(void) { return g_last_error.c_str(); }
 
 int la_last_launch_count(void) { return g_state.last_launches; }
+
+la_status la_kernel_times(double *split_ms, double *gemm_ms, int *gemm_launches) {
+    if (!split_ms || !gemm_ms || !gemm_launches) return fail(LA_ERR_INVALID_VALUE, "NULL output pointer");
+    double t[2] = {0.0, 0.0};
+    int ng = 0;
+    la_status s = LA_OK;
+    for (auto &sp : g_spans) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(sp.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, sp.a, sp.b);
+        if (e != cudaSuccess && s == LA_OK) s = cuda_fail(e, "cudaEventElapsedTime", __FILE__, __LINE__);
+        t[sp.kind] += ms;
+        ng += sp.kind == TIMED_GEMM;
+        g_free_ev.push_back(sp.a);
+        g_free_ev.push_back(sp.b);
+    }
+    g_spans.clear();
+    *split_ms = t[0];
+    *gemm_ms = t[1];
+    *gemm_launches = ng;
+    return s;
+}
 
 }  // extern "C"

@@ -17,14 +17,21 @@ struct State {
     cudaMemPool_t pool = nullptr;
     la_mode mode = LA_MODE_3XTF32;
     // Accumulator promotion interval in K elements (0 = whole K in TMEM).
-    // Default decided by the tcgen05 accumulation probe (App. C).
-    int64_t promote_k = 0;
+    // Default 256: the tcgen05 kind::tf32 accumulator truncates (probe in
+    // tests/test_probe.py); promotion every 256 keeps 3xTF32 at ~0.06 x 2^-20 S.
+    int64_t promote_k = 256;
     int64_t max_sms = 0;
     int64_t panels = 4;
     int last_launches = 0;
     void *staging = nullptr;  // la_gemm_host device staging
     size_t staging_bytes = 0;
+    bool kernel_timing = false;
 };
+
+// Event pairs bracketing split and GEMM launches (LA_OPT_KERNEL_TIMING).
+enum TimedKind { TIMED_SPLIT = 0, TIMED_GEMM = 1 };
+la_status timing_begin(cudaStream_t st, cudaEvent_t *ev);
+la_status timing_end(cudaStream_t st, cudaEvent_t ev, TimedKind kind);
 
 extern State g_state;
 extern std::mutex g_mutex;

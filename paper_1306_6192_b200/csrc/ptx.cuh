@@ -49,10 +49,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+// Spin until the phase with the given parity has completed.  A watchdog turns
+// a protocol bug into a trap (an error the host sees) instead of a hung GPU:
+// no wait in this library legitimately lasts anywhere near 2^36 cycles.
+__device__ __forceinline__ void mbar_watchdog(uint64_t t0) {
+    if (clock64() - t0 > (1ll << 36)) __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     uint32_t done;
-    do {
+    uint64_t t0 = 0;
+    for (uint32_t it = 0;; it++) {
         asm volatile(
             "{\n\t.reg .pred P;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
@@ -60,7 +67,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "=r"(done)
             : "r"(a), "r"(parity)
             : "memory");
-    } while (!done);
+        if (done) return;
+        if (it == 0) t0 = clock64();
+        else if ((it & 1023) == 0) mbar_watchdog(t0);
+    }
+}
+// Same, with cluster-scope acquire (arrivals come from the peer CTA).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done;
+    uint64_t t0 = 0;
+    for (uint32_t it = 0;; it++) {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (it == 0) t0 = clock64();
+        else if ((it & 1023) == 0) mbar_watchdog(t0);
+    }
+}
+// Arrive on the barrier at the same offset in CTA 0 of the cluster (CG == 2),
+// or on the local one (CG == 1).
+template <int CG>
+__device__ __forceinline__ void mbar_arrive_cta0(uint64_t *bar) {
+    if constexpr (CG == 1) mbar_arrive(bar);
+    else mbar_arrive_cluster(bar, 0);
 }
 
 // ---------------------------------------------------------------- TMA

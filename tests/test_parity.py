@@ -37,7 +37,8 @@ def la():
 def _gpu(la, A, B, mode="3xtf32"):
     la.set_mode(mode)
     try:
-        C = la.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+        C = la.gemm(torch.from_numpy(np.ascontiguousarray(A)).cuda(),
+                    torch.from_numpy(np.ascontiguousarray(B)).cuda())
         torch.cuda.synchronize()
     finally:
         la.set_mode("3xtf32")
