@@ -88,7 +88,7 @@ class Clocks:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
                 stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -358,6 +358,8 @@ def run_ours(a, rank, world, local_rank):
                          f"in {dt:.1f} s, Listing 1 in C (-O2 -ffp-contract=off), {threads} threads"}
 
     clocks = clk.summary()
+    if clocks.get("sm_mhz"):
+        roofline["frac_of_clock_limited_tf32"] = achieved / (148 * 4096 * clocks["sm_mhz"] * 1e6 / 1e12)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
