@@ -204,18 +204,26 @@ def comm_init(uid: bytes, rank: int, ngpu: int) -> None:
     _check(_lib.la_comm_init(buf, int(rank), int(ngpu)), "la_comm_init")
 
 
-def comm_init_from_process_group(group=None) -> None:
-    """Bootstrap the library's NCCL communicator over an initialised
-    torch.distributed process group (rank 0 creates the id, broadcast over the
-    group, every rank calls la_comm_init)."""
+def bootstrap_unique_id(group=None) -> bytes:
+    """Rank 0 of an initialised torch.distributed group creates the NCCL unique
+    id (la_get_unique_id); it is broadcast over the group; every rank returns
+    the same 128 bytes."""
     import torch
     import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rank = dist.get_rank(group)
     uid = get_unique_id() if rank == 0 else bytes(128)
     dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
     t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
     dist.broadcast(t, src=0, group=group)
-    comm_init(bytes(t.cpu().tolist()), rank, world)
+    return bytes(t.cpu().tolist())
+
+
+def comm_init_from_process_group(group=None) -> None:
+    """Create the library's NCCL communicator over an initialised
+    torch.distributed process group (one process per GPU)."""
+    import torch.distributed as dist
+    uid = bootstrap_unique_id(group)
+    comm_init(uid, dist.get_rank(group), dist.get_world_size(group))
 
 
 def gemm_multi(n, m, p, A_local, B, C_local, C_full=None, root=0, ngpu=1, stream=None):

@@ -209,7 +209,8 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
-    args.group_m = 16;
+    static const int group_env = getenv("LA_GROUP_M") ? atoi(getenv("LA_GROUP_M")) : 0;
+    args.group_m = group_env > 0 ? group_env : 16;
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
 
     auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES>;

@@ -1,0 +1,113 @@
+"""Multi-GPU partition.
+
+This run has one GPU, so:
+  * the host-side logic of the partition runs in a world-size-2 gloo group on
+    the CPU: the NCCL unique-id bootstrap, the row sharding (la_shard_rows) and
+    the reassembly of C from row shards (each rank multiplies its shard with the
+    oracle, the shards are all-gathered and must equal the full product);
+  * the device path of la_gemm_multi (panel packing, ncclBroadcast of B,
+    per-panel split + GEMM into column blocks of C, ncclAllGather) runs on one
+    B200 with a 1-rank communicator and must be bitwise equal to la_gemm.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import inputs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        import paper_1306_6192_b200 as la
+        # 1. unique-id bootstrap: every rank sees rank 0's id
+        uid = la.bootstrap_unique_id()
+        ids = [None] * world
+        dist.all_gather_object(ids, uid)
+        assert all(x == ids[0] for x in ids) and len(uid) == 128 and any(uid)
+        # 2. row sharding + reassembly of C, n not divisible by world
+        n, m, p = 37, 50, 23
+        row0, rows = la.shard_rows(n, rank, world)
+        A = inputs.generate(n, m, 0, "integer", row_idx=list(range(row0, row0 + rows))).numpy()
+        B = inputs.generate(m, p, 1, "integer").numpy()
+        Cr = oracle.gemm(A, B)
+        parts = [None] * world
+        dist.all_gather_object(parts, (row0, Cr))
+        full = np.concatenate([c for _, c in sorted(parts, key=lambda x: x[0])])
+        Afull, _ = inputs.pair(n, m, p, "integer")
+        assert np.array_equal(full, oracle.gemm(Afull.numpy(), B))
+        # 3. max over ranks (bench timing rule)
+        t = torch.tensor([float(rank + 1)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        assert t.item() == world
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as ex:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(ex)))
+
+
+def test_gloo_world2_host_logic():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
+
+
+@pytest.fixture(scope="module")
+def la1():
+    import paper_1306_6192_b200 as la
+    la.init(0)
+    la.comm_init(la.get_unique_id(), 0, 1)
+    yield la
+    la.set_option("panels", 4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,p,panels", [(512, 384, 640, 1), (512, 384, 640, 3), (300, 1000, 1500, 4),
+                                          (4096, 2048, 4096, 4)])
+def test_multi_one_rank_bitwise_equals_single(la1, n, m, p, panels):
+    la = la1
+    la.set_option("panels", panels)
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    ref = la.gemm(A, B)
+    Cl = torch.empty(n, p, device="cuda")
+    Cf = torch.empty(n, p, device="cuda")
+    la.gemm_multi(n, m, p, A, B, Cl, Cf, root=0, ngpu=1)
+    torch.cuda.synchronize()
+    assert torch.equal(Cl, ref)
+    assert torch.equal(Cf, ref)
+    pc = -(-(-(-p // panels)) // 128) * 128            # panel width: ceil(p / panels) up to 128
+    n_panels = -(-p // pc)
+    assert la.last_launch_count() == 1 + 2 * n_panels   # split A, then split B + GEMM per panel
+
+
+@pytest.mark.gpu
+def test_multi_errors(la1):
+    la = la1
+    A = torch.zeros(8, 8, device="cuda")
+    with pytest.raises(la.LaError):
+        la.gemm_multi(8, 8, 8, A, A, torch.empty(8, 8, device="cuda"), None, root=0, ngpu=2)
+    with pytest.raises(la.LaError):
+        la.gemm_multi(8, 8, 8, A, None, torch.empty(8, 8, device="cuda"), None, root=0, ngpu=1)
