@@ -40,7 +40,7 @@ namespace la {
 
 constexpr int BK = 32;            // K per stage: 32 fp32 = one 128-byte swizzle row
 constexpr int ROWS_PER_CTA = 128; // UMMA M per CTA
-constexpr int NUM_CTRL_WARPS = 4; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 idle
+constexpr int NUM_CTRL_WARPS = 4; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 tile scheduler
 constexpr int NUM_EPI_WARPS = 8;  // two per TMEM lane quarter (column halves)
 constexpr int NUM_THREADS = 32 * (NUM_CTRL_WARPS + NUM_EPI_WARPS);
 // setmaxnreg budgets.  A CTA's register pool is what it was launched with:
@@ -60,6 +60,25 @@ struct GemmArgs {
     int32_t num_kb;     // K-blocks of BK
     int32_t kc;         // K-blocks per TMEM chunk (promotion interval); >= num_kb: no promotion
     int32_t tiles_m, tiles_n, group_m;
+    int32_t use_clc;    // 1: one cluster per tile + cluster launch control; 0: static persistent stride
+};
+
+constexpr int SCHED_SLOTS = 4;  // tile ids the scheduler may hand out ahead of the slowest role
+
+// Consumer side of the tile-id ring: every role warp reads every slot once and
+// releases it on the leader CTA's sched_empty barrier.
+template <int CG>
+struct SchedReader {
+    int slot = 0;
+    uint32_t ph = 0;
+    __device__ __forceinline__ int next(uint64_t *sfull, uint64_t *sempty, const int32_t *stile, uint32_t lane) {
+        ptx::mbar_wait_cluster(&sfull[slot], ph);
+        const int t = *reinterpret_cast<const volatile int32_t *>(&stile[slot]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cta0<CG>(&sempty[slot]);
+        if (++slot == SCHED_SLOTS) { slot = 0; ph ^= 1; }
+        return t;
+    }
 };
 
 template <int CG, int BN, int STAGES, int PASSES>
@@ -71,7 +90,7 @@ struct GemmCfg {
     static constexpr int B_TILE = B_ROWS * BK * 4;
     static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);  // per CTA
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * 32 * 32 * 4; // per-warp transpose buffers
-    static constexpr int BAR_BYTES = 256;
+    static constexpr int BAR_BYTES = 512;  // mbarriers, TMEM address, tile ids; CLC response at +256
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
     static constexpr int COLS_PER_WARP = BN / 2;   // epilogue column half
@@ -133,7 +152,12 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *sfull = tempty + 2;              // [SCHED_SLOTS] tile id ready (each CTA)
+    uint64_t *sempty = sfull + SCHED_SLOTS;    // [SCHED_SLOTS] tile id consumed (leader)
+    uint64_t *clc_bar = sempty + SCHED_SLOTS;  // cluster-launch-control response ready
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(clc_bar + 1);
+    int32_t *stile = reinterpret_cast<int32_t *>(tmem_holder + 4);         // [SCHED_SLOTS]
+    uint8_t *clc_resp = reinterpret_cast<uint8_t *>(full) + 256;          // 16 B, 16-B aligned
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -158,6 +182,11 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&tfull[b], 1);                      // one tcgen05.commit
             ptx::mbar_init(&tempty[b], CG * NUM_EPI_WARPS);    // one arrive per epilogue warp of the pair
         }
+        for (int i = 0; i < SCHED_SLOTS; i++) {
+            ptx::mbar_init(&sfull[i], 1);                              // scheduler's remote arrive
+            ptx::mbar_init(&sempty[i], CG + 1 + CG * NUM_EPI_WARPS);  // producers, MMA, epilogue warps
+        }
+        ptx::mbar_init(clc_bar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_holder, Cfg::TMEM_COLS);
@@ -179,7 +208,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint64_t pol = ptx::policy_evict_normal();
         int s = 0;
         uint32_t ph = 0;
-        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        SchedReader<CG> sched;
+        for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
             int tm, tn;
             tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
             const int32_t m0 = tm * Cfg::TILE_M + rank * ROWS_PER_CTA;
@@ -209,12 +239,51 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
+    } else if (warp == 3 && rank == 0) {
+        // ======================= tile scheduler (leader CTA) =======================
+        // Hands tile ids to every role of both CTAs through the sfull/sempty
+        // ring.  With use_clc the grid has one cluster per tile: the first tile
+        // is this cluster's own, later ones are claimed by cancelling clusters
+        // the hardware has not launched yet (cluster launch control), so the
+        // tiles in flight stay a compact window of the raster order (L2 reuse)
+        // and faster SM pairs simply take more tiles.
+        int slot = 0;
+        uint32_t ph = 0, cph = 0;
+        int t = cluster_id;
+        for (;;) {
+            if (t >= num_tiles) t = -1;
+            ptx::mbar_wait_cluster(&sempty[slot], ph ^ 1);
+            if (lane == 0) {
+#pragma unroll
+                for (uint32_t r = 0; r < CG; r++) {
+                    ptx::st_shared_cluster_u32(&stile[slot], r, (uint32_t)t);
+                    ptx::mbar_arrive_cluster(&sfull[slot], r);
+                }
+            }
+            __syncwarp();
+            if (++slot == SCHED_SLOTS) { slot = 0; ph ^= 1; }
+            if (t < 0) break;
+            if (args.use_clc) {
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(clc_bar, 16);
+                    ptx::clc_try_cancel(clc_resp, clc_bar);
+                }
+                __syncwarp();
+                ptx::mbar_wait(clc_bar, cph);
+                cph ^= 1;
+                const int32_t x = ptx::clc_query(clc_resp);
+                t = x < 0 ? -1 : x / CG;
+            } else {
+                t += num_clusters;
+            }
+        }
     } else if (warp == 1 && rank == 0) {
         // ======================= MMA issuer (leader CTA) =======================
         constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::TILE_M, BN);
         int s = 0;
         uint32_t ph = 0, buf = 0, aph = 0;
-        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        SchedReader<CG> sched;
+        for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
             for (int kb = 0; kb < num_kb; kb++) {
                 const int kin = kb % kc;
                 const bool chunk_first = kin == 0;
@@ -268,7 +337,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t tq = tmem_base + ((32u * q) << 16) + half * Cfg::COLS_PER_WARP;
         uint32_t buf = 0, aph = 0;
         const int nchunks = (num_kb + kc - 1) / kc;
-        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        SchedReader<CG> sched;
+        for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
             int tm, tn;
             tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
             const int64_t row0 = (int64_t)tm * Cfg::TILE_M + rank * ROWS_PER_CTA + 32 * q;

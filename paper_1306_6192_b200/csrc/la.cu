@@ -209,7 +209,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
-    static const int group_env = getenv("LA_GROUP_M") ? atoi(getenv("LA_GROUP_M")) : 0;
+    const int group_env = getenv("LA_GROUP_M") ? atoi(getenv("LA_GROUP_M")) : 0;  // experiment knob
     args.group_m = group_env > 0 ? group_env : 16;
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
 
@@ -237,9 +237,19 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         }
         max_clusters = nc;
     }
+    // Default: one cluster per tile, dynamically re-distributed by cluster
+    // launch control (see the kernel's scheduler warp).  When the caller caps
+    // the SMs (multi-GPU overlap with NCCL), a static persistent grid of at
+    // most max_sms SMs instead, because CLC cannot bound residency.
     int clusters = max_clusters;
+    const bool env_static = getenv("LA_STATIC_SCHED") && atoi(getenv("LA_STATIC_SCHED")) != 0;
+    args.use_clc = (max_sms <= 0 && !env_static) ? 1 : 0;
     if (max_sms > 0) clusters = std::min(clusters, std::max(1, max_sms / CG));
     clusters = (int)std::min<int64_t>(tiles, clusters);
+    if (args.use_clc) {
+        if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
+        clusters = (int)tiles;
+    }
     cudaEvent_t t0;
     if ((s = timing_begin(st, &t0)) != LA_OK) return s;
     kern<<<clusters * CG, NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, args);
