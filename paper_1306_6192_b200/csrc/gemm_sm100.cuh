@@ -61,7 +61,28 @@ struct GemmArgs {
     int32_t kc;         // K-blocks per TMEM chunk (promotion interval); >= num_kb: no promotion
     int32_t tiles_m, tiles_n, group_m;
     int32_t use_clc;    // 1: one cluster per tile + cluster launch control; 0: static persistent stride
+    int32_t *wave_sync; // static stride only, optional: per-wave arrival counters (zeroed per launch)
 };
+
+// Optional K-phase alignment of the static persistent schedule: before the
+// first load of its w-th tile every producer arrives on counter w and waits
+// (bounded, 200 us) until all producers of that wave have arrived, so the
+// clusters that share A rows / B columns stream through K together and reuse
+// each other's slabs in L2 instead of re-reading them from HBM.
+__device__ __forceinline__ void wave_barrier(int32_t *ctr, int target) {
+    atomicAdd(ctr, 1);
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        int v;
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        if (v >= target) break;
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 200000) break;
+        __nanosleep(128);
+    }
+}
 
 constexpr int SCHED_SLOTS = 4;  // tile ids the scheduler may hand out ahead of the slowest role
 
@@ -214,6 +235,11 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
             const int32_t m0 = tm * Cfg::TILE_M + rank * ROWS_PER_CTA;
             const int32_t n0 = tn * BN + rank * Cfg::B_ROWS;
+            if (args.wave_sync != nullptr) {
+                const int w = t / num_clusters;
+                if (lane == 0) wave_barrier(args.wave_sync + w, CG * min(num_clusters, num_tiles - w * num_clusters));
+                __syncwarp();
+            }
             for (int kb = 0; kb < num_kb; kb++) {
                 ptx::mbar_wait(&empty[s], ph ^ 1);
                 if (lane == 0) {

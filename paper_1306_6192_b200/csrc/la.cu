@@ -237,18 +237,32 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         }
         max_clusters = nc;
     }
-    // Default: one cluster per tile, dynamically re-distributed by cluster
-    // launch control (see the kernel's scheduler warp).  When the caller caps
-    // the SMs (multi-GPU overlap with NCCL), a static persistent grid of at
-    // most max_sms SMs instead, because CLC cannot bound residency.
+    // Default: a static persistent grid (one cluster per SM pair, tiles strided
+    // in grouped raster order).  LA_CLC=1 instead launches one cluster per tile
+    // and lets running clusters claim pending ones through cluster launch
+    // control (dynamic balancing) -- measured: 129 GB of DRAM reads per n=16384
+    // launch vs 105-113 GB static, because dynamically started tiles drift
+    // apart in K and share fewer L2 slabs (profiles/ncu_r01_sched_ab.md).  CLC
+    // is never used when the caller caps the SMs (it cannot bound residency).
     int clusters = max_clusters;
-    const bool env_static = getenv("LA_STATIC_SCHED") && atoi(getenv("LA_STATIC_SCHED")) != 0;
-    args.use_clc = (max_sms <= 0 && !env_static) ? 1 : 0;
+    const bool env_clc = getenv("LA_CLC") && atoi(getenv("LA_CLC")) != 0;
+    args.use_clc = (max_sms <= 0 && env_clc) ? 1 : 0;
     if (max_sms > 0) clusters = std::min(clusters, std::max(1, max_sms / CG));
     clusters = (int)std::min<int64_t>(tiles, clusters);
     if (args.use_clc) {
         if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
         clusters = (int)tiles;
+    }
+    args.wave_sync = nullptr;
+    void *sync_buf = nullptr;
+    const bool env_wave = getenv("LA_WAVE_SYNC") && atoi(getenv("LA_WAVE_SYNC")) != 0;
+    if (!args.use_clc && env_wave) {
+        const size_t nw = (size_t)((tiles + clusters - 1) / clusters);
+        cudaError_t e = cudaMallocFromPoolAsync(&sync_buf, nw * sizeof(int32_t), g_state.pool, st);
+        if (e != cudaSuccess) return cuda_fail(e, "wave sync buffer", __FILE__, __LINE__);
+        e = cudaMemsetAsync(sync_buf, 0, nw * sizeof(int32_t), st);
+        if (e != cudaSuccess) return cuda_fail(e, "wave sync memset", __FILE__, __LINE__);
+        args.wave_sync = static_cast<int32_t *>(sync_buf);
     }
     cudaEvent_t t0;
     if ((s = timing_begin(st, &t0)) != LA_OK) return s;
@@ -256,6 +270,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
+    if (sync_buf) cudaFreeAsync(sync_buf, st);
     return timing_end(st, t0, TIMED_GEMM);
 }
 
