@@ -110,9 +110,12 @@ LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, cons
 
 /* End-to-end variant on HOST buffers (the paper's host flow):
  * copies h_A and h_B to the device, computes, copies C back into h_C and
- * synchronises `stream` before returning.  Host buffers may be pageable or
- * pinned (pinned is faster).  Device staging is library-owned and reused
- * across calls.  Errors: as la_gemm. */
+ * returns after everything completed.  The copies are pipelined with the
+ * compute: B first, then A in row panels on a copy-in stream, each panel's
+ * split + GEMM on `stream` as soon as it lands, each C panel copied back on a
+ * copy-out stream while later panels compute.  Results are bitwise identical
+ * to la_gemm.  Host buffers may be pageable or pinned (only pinned buffers
+ * overlap).  Device staging is library-owned and reused.  Errors: as la_gemm. */
 LA_API la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B,
                        float *h_C, void *stream);
 

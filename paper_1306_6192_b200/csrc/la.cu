@@ -432,6 +432,13 @@ la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float
     return s;
 }
 
+// End-to-end product on host buffers, pipelined (the paper's host flow, P:23
+// and P:144, with the transfer the paper calls the weak point hidden behind
+// compute): B goes first (every output row needs all of it), then A in row
+// panels on a copy-in stream; the caller's stream splits B once and then, per
+// panel, splits the A rows and runs the GEMM on them as soon as they land; a
+// copy-out stream returns each C panel while later panels compute.  With
+// pinned host buffers the copies overlap compute in both directions.
 la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
                        void *stream) {
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
@@ -440,9 +447,13 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t ab = (size_t)(n * m) * 4, bb = (size_t)(m * p) * 4, cb = (size_t)(n * p) * 4;
     const size_t need = ab + bb + cb + 3 * 256;
+    if (!g_state.h2d) {
+        LA_CK(cudaStreamCreateWithFlags(&g_state.h2d, cudaStreamNonBlocking));
+        LA_CK(cudaStreamCreateWithFlags(&g_state.d2h, cudaStreamNonBlocking));
+    }
     if (g_state.staging_bytes < need) {
         if (g_state.staging) {
-            LA_CK(cudaStreamSynchronize(st));
+            LA_CK(cudaDeviceSynchronize());
             LA_CK(cudaFree(g_state.staging));
             g_state.staging = nullptr;
             g_state.staging_bytes = 0;
@@ -458,13 +469,65 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     float *dA = reinterpret_cast<float *>(base);
     float *dB = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256);
     float *dC = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256 + (bb + 255) / 256 * 256);
-    LA_CK(cudaMemcpyAsync(dA, h_A, ab, cudaMemcpyHostToDevice, st));
-    LA_CK(cudaMemcpyAsync(dB, h_B, bb, cudaMemcpyHostToDevice, st));
+
+    // row panels: 8 for big problems (multiples of the 256-row tile), else 1
+    const int64_t panel_rows = n >= 2048 ? ((n + 7) / 8 + 255) / 256 * 256 : n;
+    const int64_t P = (n + panel_rows - 1) / panel_rows;
+    while ((int64_t)g_state.host_events.size() < 2 * P + 2) {
+        cudaEvent_t e;
+        LA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        g_state.host_events.push_back(e);
+    }
+    cudaEvent_t ev_start = g_state.host_events[0], ev_b = g_state.host_events[1];
+    cudaEvent_t *ev_a = &g_state.host_events[2], *ev_c = &g_state.host_events[2 + P];
+
+    const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&ws, operands_bytes(n, m, p, passes), g_state.pool, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LA_ERR_OUT_OF_MEMORY, "workspace");
+    }
+    const Operands ops = operands_carve(ws, n, m, p, passes);
     int launches = 0;
-    la_status s = gemm_impl(n, m, p, dA, dB, dC, p, st, &launches);
+
+    // the copy-in stream starts after everything already queued on `st`
+    LA_CK(cudaEventRecord(ev_start, st));
+    LA_CK(cudaStreamWaitEvent(g_state.h2d, ev_start, 0));
+    LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_start, 0));
+    LA_CK(cudaMemcpyAsync(dB, h_B, bb, cudaMemcpyHostToDevice, g_state.h2d));
+    LA_CK(cudaEventRecord(ev_b, g_state.h2d));
+    for (int64_t i = 0; i < P; i++) {
+        const int64_t r0 = i * panel_rows, rows = std::min(panel_rows, n - r0);
+        LA_CK(cudaMemcpyAsync(dA + r0 * m, h_A + r0 * m, (size_t)(rows * m) * 4, cudaMemcpyHostToDevice,
+                              g_state.h2d));
+        LA_CK(cudaEventRecord(ev_a[i], g_state.h2d));
+    }
+    LA_CK(cudaStreamWaitEvent(st, ev_b, 0));
+    la_status s = split_b(m, 0, p, dB, p, ops, st, &launches);
+    for (int64_t i = 0; i < P && s == LA_OK; i++) {
+        const int64_t r0 = i * panel_rows, rows = std::min(panel_rows, n - r0);
+        LA_CK(cudaStreamWaitEvent(st, ev_a[i], 0));
+        Operands pan = ops;
+        pan.a_hi = ops.a_hi + r0 * ops.mp;
+        pan.a_lo = ops.a_lo + r0 * ops.mp;
+        s = split_a(rows, m, dA + r0 * m, pan, st, &launches);
+        if (s == LA_OK) s = gemm_run(rows, m, 0, p, pan, dC + r0 * p, p, (int)g_state.max_sms, st, &launches);
+        if (s == LA_OK) {
+            LA_CK(cudaEventRecord(ev_c[i], st));
+            LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_c[i], 0));
+            LA_CK(cudaMemcpyAsync(h_C + r0 * p, dC + r0 * p, (size_t)(rows * p) * 4, cudaMemcpyDeviceToHost,
+                                  g_state.d2h));
+        }
+    }
+    cudaFreeAsync(ws, st);
     g_state.last_launches = launches;
-    if (s != LA_OK) return s;
-    LA_CK(cudaMemcpyAsync(h_C, dC, cb, cudaMemcpyDeviceToHost, st));
+    if (s != LA_OK) {
+        cudaStreamSynchronize(g_state.h2d);
+        cudaStreamSynchronize(g_state.d2h);
+        return s;
+    }
+    LA_CK(cudaStreamSynchronize(g_state.d2h));
     LA_CK(cudaStreamSynchronize(st));
     return LA_OK;
 }
@@ -485,6 +548,11 @@ la_status la_finalize(void) {
     la_status s = comm_destroy();
     if (g_state.staging) cudaFree(g_state.staging);
     g_state.staging = nullptr;
+    for (auto e : g_state.host_events) cudaEventDestroy(e);
+    g_state.host_events.clear();
+    if (g_state.h2d) cudaStreamDestroy(g_state.h2d);
+    if (g_state.d2h) cudaStreamDestroy(g_state.d2h);
+    g_state.h2d = g_state.d2h = nullptr;
     g_state.staging_bytes = 0;
     if (g_state.pool) cudaMemPoolDestroy(g_state.pool);
     g_state.pool = nullptr;

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "la.h"
 
@@ -26,6 +27,8 @@ struct State {
     void *staging = nullptr;  // la_gemm_host device staging
     size_t staging_bytes = 0;
     bool kernel_timing = false;
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // la_gemm_host copy streams
+    std::vector<cudaEvent_t> host_events;
 };
 
 // Event pairs bracketing split and GEMM launches (LA_OPT_KERNEL_TIMING).

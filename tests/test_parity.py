@@ -162,6 +162,20 @@ def test_host_entry_point(la):
     assert np.array_equal(Cp.numpy(), C)
 
 
+@pytest.mark.parametrize("n,m,p", [(2300, 700, 900), (4096, 1024, 2048)])
+def test_host_entry_point_pipelined_panels(la, n, m, p):
+    """n >= 2048 takes the pipelined row-panel path (ragged last panel at 2300)."""
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    ref = la.gemm(A, B).cpu()
+    Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
+    Ch = torch.empty(n, p).pin_memory()
+    la.gemm_host(Ah, Bh, out=Ch)
+    assert torch.equal(Ch, ref)
+    rows = [0, 511, 512, n - 1]
+    _check(inputs.generate(n, m, 0, "stress", row_idx=rows).numpy(), B.cpu().numpy(),
+           Ch.numpy()[rows], "stress", "3xtf32")
+
+
 def test_error_paths_on_gpu(la):
     A = torch.zeros(4, 4, device="cuda")
     lib = la._lib
