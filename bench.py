@@ -73,63 +73,57 @@ def _peaks():
 
 # ----------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples SM clock, power and throttle reasons every 20 ms during the timed
+    region with NVML (the library nvidia-smi reads); falls back to nvidia-smi."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.path = None
+        self.samples = []
+        self._stop = False
+        self._thread = None
+
+    def _run(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, pw, rs))
+            except Exception:
+                pass
+            time.sleep(0.02)
 
     def __enter__(self):
+        import threading
+        self.max_mhz = None
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
-                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            import pynvml  # noqa: F401
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+            time.sleep(0.005)
         except Exception:
-            self.proc = None
-        time.sleep(0.3)
+            self._thread = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop = True
+        if self._thread is not None:
+            self._thread.join(timeout=2)
 
     def summary(self):
-        rows = []
-        try:
-            for line in open(self.path):
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 7:
-                    rows.append(parts)
-        except Exception:
-            pass
-        finally:
-            if self.path and os.path.exists(self.path):
-                os.unlink(self.path)
-        if not rows:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        power = [num(r[2]) or 0.0 for r in rows]
-        pmax = max(power)
-        loaded = [r for r, pw in zip(rows, power) if pw >= 0.5 * pmax] or rows
-        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][1]),
-                "reasons": reasons, "samples": len(rows), "power_w_max": pmax}
+        sm = [x[0] for x in self.samples]
+        reasons = sorted({name for _, _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "power_w_max": max(x[1] for x in self.samples),
+                "power_w_median": statistics.median(x[1] for x in self.samples), "source": "NVML, 20 ms"}
 
 
 # ----------------------------------------------------------------- oracle sample (CPU)
@@ -244,10 +238,10 @@ def run_ours(a, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     with Clocks(local_rank) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
         ev0.record(stream)
         for _ in range(a.steps):
             step()
