@@ -68,10 +68,11 @@ typedef enum {
 } la_mode;
 
 typedef enum {
-    /* K elements accumulated in tensor memory before the partial sum is added
-     * into an fp32 register running sum (round-to-nearest).  0 = never (the whole
-     * K range accumulates in TMEM).  Rounded up to a multiple of 32.  Default:
-     * chosen from the accumulator-rounding probe, see DESIGN.md. */
+    /* 3xTF32 only: K elements accumulated in tensor memory before the partial
+     * sum is added into an fp32 register running sum (round-to-nearest).  0 =
+     * never (the whole K range accumulates in TMEM).  Rounded up to a multiple
+     * of 32.  Default 256: the tcgen05 tf32 accumulator truncates, and whole-K
+     * accumulation breaks the 2^-20 bound. */
     LA_OPT_PROMOTE_K = 0,
     /* Upper bound on the number of SMs the GEMM kernel occupies (0 = all).  The
      * multi-GPU path uses it to leave SMs for NCCL. */
