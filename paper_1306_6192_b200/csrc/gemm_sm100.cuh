@@ -61,7 +61,10 @@ struct GemmArgs {
     int32_t kc;         // K-blocks per TMEM chunk (promotion interval); >= num_kb: no promotion
     int32_t tiles_m, tiles_n, group_m;
     int32_t use_clc;    // 1: one cluster per tile + cluster launch control; 0: static persistent stride
-    int32_t *wave_sync; // static stride only, optional: per-wave arrival counters (zeroed per launch)
+    int32_t *wave_sync; // static stride only, optional: arrival counters (zeroed per launch), one per
+                        // (wave, K phase of sync_kb K-blocks)
+    int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
+    int32_t debug;      // diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip MMAs
 };
 
 // Optional K-phase alignment of the static persistent schedule: before the
@@ -235,14 +238,18 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
             const int32_t m0 = tm * Cfg::TILE_M + rank * ROWS_PER_CTA;
             const int32_t n0 = tn * BN + rank * Cfg::B_ROWS;
-            if (args.wave_sync != nullptr) {
-                const int w = t / num_clusters;
-                if (lane == 0) wave_barrier(args.wave_sync + w, CG * min(num_clusters, num_tiles - w * num_clusters));
-                __syncwarp();
-            }
+            const int wave = t / num_clusters;
+            const int wave_target = CG * min(num_clusters, num_tiles - wave * num_clusters);
+            const int phases = (num_kb + args.sync_kb - 1) / args.sync_kb;
             for (int kb = 0; kb < num_kb; kb++) {
+                if (args.wave_sync != nullptr && kb % args.sync_kb == 0) {
+                    if (lane == 0) wave_barrier(args.wave_sync + wave * phases + kb / args.sync_kb, wave_target);
+                    __syncwarp();
+                }
                 ptx::mbar_wait(&empty[s], ph ^ 1);
-                if (lane == 0) {
+                if (lane == 0 && (args.debug & 1)) {
+                    if (rank == 0) ptx::mbar_arrive(&full[s]);
+                } else if (lane == 0) {
                     const int32_t k0 = kb * BK;
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], CG * Cfg::STAGE_BYTES);
                     if constexpr (CG == 1) {
@@ -323,6 +330,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 ptx::tc_fence_after();
                 if (lane == 0) {
                     const uint32_t d = tmem_base + buf * BN;
+                    if (!(args.debug & 2)) {
                     const uint32_t ah = ptx::smem_u32(a_tile(s, 0)), bh = ptx::smem_u32(b_tile(s, 0));
                     const uint32_t al = ptx::smem_u32(a_tile(s, PASSES == 3 ? 1 : 0));
                     const uint32_t bl = ptx::smem_u32(b_tile(s, PASSES == 3 ? 1 : 0));
@@ -340,6 +348,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         } else {
                             ptx::mma_tf32<CG>(d, dah, dbh, idesc, acc);
                         }
+                    }
                     }
                     ptx::mma_commit<CG>(&empty[s]);
                     if (chunk_last) ptx::mma_commit<CG>(&tfull[buf]);

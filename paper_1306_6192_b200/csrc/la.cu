@@ -212,7 +212,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
     const int group_env = getenv("LA_GROUP_M") ? atoi(getenv("LA_GROUP_M")) : 0;  // experiment knob
-    args.group_m = group_env > 0 ? group_env : 16;
+    args.group_m = group_env > 0 ? group_env : 8;
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
 
     auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES>;
@@ -255,11 +255,23 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
         clusters = (int)tiles;
     }
+    args.debug = getenv("LA_DEBUG_KERNEL") ? atoi(getenv("LA_DEBUG_KERNEL")) : 0;  // diagnostics only
     args.wave_sync = nullptr;
+    args.sync_kb = args.num_kb;
     void *sync_buf = nullptr;
-    const bool env_wave = getenv("LA_WAVE_SYNC") && atoi(getenv("LA_WAVE_SYNC")) != 0;
-    if (!args.use_clc && env_wave) {
-        const size_t nw = (size_t)((tiles + clusters - 1) / clusters);
+    // K-phase alignment of the static schedule (gemm_sm100.cuh wave_barrier):
+    // every 16 K-blocks the producers of a wave meet at a counter, so clusters
+    // that share A rows / B columns stream K together and hit each other's
+    // slabs in L2.  Measured at n = 16384: DRAM reads 105-129 GB -> 42 GB per
+    // launch, 13% less energy and +14% sustained throughput under the power cap
+    // (profiles/energy_r01.md).  On by default for multi-wave problems with a
+    // long K; LA_WAVE_SYNC=0 disables, =N sets the interval in K-blocks.
+    const char *ws_env = getenv("LA_WAVE_SYNC");
+    int wave_sync = ws_env ? atoi(ws_env) : (tiles >= clusters && args.num_kb >= 64 ? 16 : 0);
+    if (!args.use_clc && wave_sync > 0) {
+        args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
+        const int64_t phases = (args.num_kb + args.sync_kb - 1) / args.sync_kb;
+        const size_t nw = (size_t)((tiles + clusters - 1) / clusters * phases);
         cudaError_t e = cudaMallocFromPoolAsync(&sync_buf, nw * sizeof(int32_t), g_state.pool, st);
         if (e != cudaSuccess) return cuda_fail(e, "wave sync buffer", __FILE__, __LINE__);
         e = cudaMemsetAsync(sync_buf, 0, nw * sizeof(int32_t), st);
