@@ -262,7 +262,9 @@ def run_ours(a, rank, world, local_rank):
 
     # roofline of the dominant kernel (the GEMM), per launch, this rank
     pk, src = _peaks()
-    tf32_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops")) * TF32_PER_BF16
+    # The GEMM is the only large kernel and is timed in a region of < 1 s, so the
+    # burst figure applies (the 4-s sustained cuBLAS bf16 loop runs ~15% lower).
+    tf32_peak = pk.get("bf16_tflops", 1590.0) * TF32_PER_BF16
     gemm_launch_ms = gemm_ms / max(1, n_gemm)
     issued_per_launch = passes * 2.0 * rows * m * p / max(1, n_gemm // a.steps)
     achieved = issued_per_launch / (gemm_launch_ms * 1e-3) / 1e12
@@ -278,7 +280,8 @@ def run_ours(a, rank, world, local_rank):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": achieved / tf32_peak, "traffic": traffic,
                 "kernel": f"gemm_tf32_sm100 ({passes} TF32 pass{'es' if passes > 1 else ''}, issued flops)",
-                "peak_source": f"{src} bf16_tflops_sustained x {TF32_PER_BF16} (nominal TF32/BF16)",
+                "peak_source": f"{src} bf16_tflops (burst) x {TF32_PER_BF16} (nominal TF32/BF16)",
+                "frac_of_sustained_peak": achieved / (pk.get("bf16_tflops_sustained", 1400.0) * TF32_PER_BF16),
                 "frac_of_tf32_datasheet": achieved / TF32_DATASHEET_TFLOPS,
                 "gemm_ms_per_launch": gemm_launch_ms, "split_ms_per_step": split_ms / a.steps,
                 "gemm_share_of_step": gemm_ms / a.steps / ms if world == 1 else None}
