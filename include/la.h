@@ -120,6 +120,27 @@ LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, cons
 LA_API la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B,
                        float *h_C, void *stream);
 
+/* Complex single-precision product (Table 2 "Complex Float" column, P:222-228;
+ * complex multiply as in SPEC S:85-93):
+ *   d_A : n x m complex64, row-major, interleaved (re, im) float pairs, device;
+ *   d_B : m x p complex64;  d_C : n x p complex64, overwritten.
+ * Computed on the same tcgen05 path as la_gemm through the real embedding
+ * [[Ar, -Ai], [Ai, Ar]] . [Br; Bi] = [Cr; Ci] (four real GEMMs of work, one
+ * launch).  Numerics as la_gemm per component, with the scales
+ * sum_r |ar||br| + |ai||bi| (real part) and sum_r |ar||bi| + |ai||br|
+ * (imaginary part).  Pointers 8-byte aligned.  Errors: as la_gemm. */
+LA_API la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B,
+                          float *d_C, void *stream);
+
+/* Matrix addition / subtraction (PAPER.md section "Rezultaty i wnioski", P:203:
+ * "Dodawanie macierzy ... 16 777 216 operacji elementarnych" at 4096 x 4096):
+ * C = A + B (subtract = 0) or C = A - B (subtract != 0), rows x cols row-major
+ * fp32, one IEEE binary32 operation per element (bitwise reproducible).  C may
+ * be A or B (in place) but must not partially overlap them.  HBM-bound
+ * (12 bytes per element).  Errors: NOT_INITIALIZED, INVALID_VALUE, CUDA. */
+LA_API la_status la_add(int64_t rows, int64_t cols, const float *d_A, const float *d_B, float *d_C,
+                        int subtract, void *stream);
+
 /* ---- multi-GPU (one process per GPU, SPMD) ------------------ */
 
 /* Rank 0 writes a 128-byte NCCL unique id into out128; the caller distributes

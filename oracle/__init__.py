@@ -20,6 +20,9 @@ abs_scale(A, B)                S_ij = sum_r |a_ir||b_rj| (binary64), the scale o
                                the north_star tolerance 2^-20 * S_ij.
 exact_grid(A, B, shift)        exact c_ij for inputs on the 2^-shift grid (int128).
 freivalds(A, B, C, x)          exact int64 Freivalds check C.x == A.(B.x).
+elementwise(A, B, subtract)    C = A + B or A - B, one binary32 op per element.
+cgemm(A, B)                    complex64 Listing 1 (Table 2 "Complex Float").
+cabs_scale(A, B)               complex tolerance scales (real part, imaginary part).
 """
 from __future__ import annotations
 
@@ -62,6 +65,12 @@ def _load():
         lib.oracle_exact_grid.restype = ctypes.c_int
         lib.oracle_freivalds_i64.argtypes = [i64, i64, i64, fp, fp, fp, fp, fp]
         lib.oracle_freivalds_i64.restype = ctypes.c_int64
+        lib.oracle_elementwise.argtypes = [i64, i64, fp, fp, fp, ctypes.c_int]
+        lib.oracle_elementwise.restype = ctypes.c_int
+        lib.oracle_cgemm.argtypes = [i64, i64, i64, fp, fp, fp]
+        lib.oracle_cgemm.restype = ctypes.c_int
+        lib.oracle_cabs_scale.argtypes = [i64, i64, i64, fp, fp, dp]
+        lib.oracle_cabs_scale.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -139,3 +148,42 @@ def freivalds(A, B, C, x) -> int:
     if bad < 0:
         raise ValueError("Freivalds needs integer-valued A, B and C")
     return int(bad)
+
+
+def elementwise(A, B, subtract: bool = False) -> np.ndarray:
+    """C = A + B (or A - B) elementwise in binary32 (P:203)."""
+    A, B = _f32(A), _f32(B)
+    if A.shape != B.shape:
+        raise ValueError("shape mismatch")
+    C = np.empty_like(A)
+    _load().oracle_elementwise(A.shape[0], A.shape[1], _ptr(A), _ptr(B), _ptr(C), int(bool(subtract)))
+    return C
+
+
+def _c64(x) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x), dtype=np.complex64)
+    if a.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    return a
+
+
+def cgemm(A, B) -> np.ndarray:
+    """Complex Listing 1: C = A.B for complex64 matrices (binary32 components)."""
+    A, B = _c64(A), _c64(B)
+    n, m = A.shape
+    m2, p = B.shape
+    if m != m2:
+        raise ValueError("inner dimension mismatch")
+    C = np.empty((n, p), dtype=np.complex64)
+    _load().oracle_cgemm(n, m, p, _ptr(A), _ptr(B), _ptr(C))
+    return C
+
+
+def cabs_scale(A, B):
+    """(Sr, Si): binary64 scales sum|ar||br|+|ai||bi| and sum|ar||bi|+|ai||br|."""
+    A, B = _c64(A), _c64(B)
+    n, m = A.shape
+    _, p = B.shape
+    S = np.empty((n, p, 2), dtype=np.float64)
+    _load().oracle_cabs_scale(n, m, p, _ptr(A), _ptr(B), _ptr(S))
+    return S[..., 0], S[..., 1]

@@ -215,3 +215,65 @@ int64_t oracle_freivalds_i64(int64_t n, int64_t m, int64_t p, const float *A,
     free(bx);
     return bad;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Matrix addition / subtraction (PAPER.md section "Rezultaty i wnioski",     */
+/* C = A +/- B, rows x cols elementary operations, 16,777,216 at       */
+/* 4096 x 4096).  One binary32 add or subtract per element, RN-even.          */
+/* ------------------------------------------------------------------------- */
+int oracle_elementwise(int64_t rows, int64_t cols, const float *A, const float *B, float *C,
+                       int subtract)
+{
+    const int64_t count = rows * cols;
+    if (subtract)
+        for (int64_t i = 0; i < count; i++) C[i] = A[i] - B[i];
+    else
+        for (int64_t i = 0; i < count; i++) C[i] = A[i] + B[i];
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Complex single-precision product (Table 2 "Complex Float";      */
+/* SPEC S:85-93 complex_mul).  Listing 1 over complex64 elements stored as    */
+/* interleaved (re, im) float pairs: for each (i, j), s = 0 + 0i, then for r  */
+/* ascending  t = a_ir * b_rj  with                                            */
+/*     t.re = fl(fl(ar*br) - fl(ai*bi)),  t.im = fl(fl(ar*bi) + fl(ai*br)),    */
+/* and s = s + t componentwise, every operation one binary32 RN operation.    */
+/* ------------------------------------------------------------------------- */
+int oracle_cgemm(int64_t n, int64_t m, int64_t p, const float *A, const float *B, float *C)
+{
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t j = 0; j < p; j++) {
+            float sr = 0.0f, si = 0.0f;
+            for (int64_t k = 0; k < m; k++) {
+                const float ar = A[2 * (i * m + k)], ai = A[2 * (i * m + k) + 1];
+                const float br = B[2 * (k * p + j)], bi = B[2 * (k * p + j) + 1];
+                const float p1 = ar * br, p2 = ai * bi, p3 = ar * bi, p4 = ai * br;
+                const float tr = p1 - p2, ti = p3 + p4;
+                sr = sr + tr;
+                si = si + ti;
+            }
+            C[2 * (i * p + j)] = sr;
+            C[2 * (i * p + j) + 1] = si;
+        }
+    return 0;
+}
+
+/* Tolerance scales for the complex product, binary64:
+ *   Sr_ij = sum_r |ar||br| + |ai||bi|,   Si_ij = sum_r |ar||bi| + |ai||br|. */
+int oracle_cabs_scale(int64_t n, int64_t m, int64_t p, const float *A, const float *B, double *S)
+{
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t j = 0; j < p; j++) {
+            double sr = 0.0, si = 0.0;
+            for (int64_t k = 0; k < m; k++) {
+                const double ar = fabs((double)A[2 * (i * m + k)]), ai = fabs((double)A[2 * (i * m + k) + 1]);
+                const double br = fabs((double)B[2 * (k * p + j)]), bi = fabs((double)B[2 * (k * p + j) + 1]);
+                sr += ar * br + ai * bi;
+                si += ar * bi + ai * br;
+            }
+            S[2 * (i * p + j)] = sr;
+            S[2 * (i * p + j) + 1] = si;
+        }
+    return 0;
+}

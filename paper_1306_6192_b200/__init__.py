@@ -28,7 +28,8 @@ OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3}
 # every symbol include/la.h declares (checked by tests/test_abi.py)
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
-           "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times")
+           "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times", "la_cgemm",
+           "la_add")
 
 
 class LaError(RuntimeError):
@@ -49,6 +50,8 @@ def _load() -> ctypes.CDLL:
         "la_get_option": ([ctypes.c_int, ctypes.POINTER(i64)], st),
         "la_gemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_gemm_host": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_cgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_add": ([i64, i64, vp, vp, vp, ctypes.c_int, vp], st),
         "la_get_unique_id": ([vp], st),
         "la_comm_init": ([vp, ctypes.c_int, ctypes.c_int], st),
         "la_gemm_multi": ([i64, i64, i64, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp], st),
@@ -150,6 +153,41 @@ def gemm(A, B, out=None, stream=None):
         if tuple(out.shape) != (n, p):
             raise ValueError("out has the wrong shape")
     _check(_lib.la_gemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_gemm")
+    return out
+
+
+def cgemm(A, B, out=None, stream=None):
+    """C = A . B for complex64 CUDA tensors (la_cgemm, Table 2 "Complex Float")."""
+    import torch
+    for t, nm in ((A, "A"), (B, "B")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.complex64:
+            raise TypeError(f"{nm} must be a complex64 CUDA tensor")
+        if t.dim() != 2 or not t.is_contiguous():
+            raise ValueError(f"{nm} must be a contiguous 2-D (row-major) matrix")
+    n, m = A.shape
+    m2, p = B.shape
+    if m != m2:
+        raise ValueError("inner dimension mismatch")
+    if out is None:
+        out = torch.empty((n, p), dtype=torch.complex64, device=A.device)
+    _check(_lib.la_cgemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_cgemm")
+    return out
+
+
+def add(A, B, out=None, subtract=False, stream=None):
+    """C = A + B (or A - B) for float32 CUDA matrices of equal shape (la_add)."""
+    import torch
+    _check_dev(A, "A")
+    _check_dev(B, "B")
+    if A.shape != B.shape:
+        raise ValueError("shape mismatch")
+    if out is None:
+        out = torch.empty_like(A)
+    else:
+        _check_dev(out, "out")
+    r, c = A.shape
+    _check(_lib.la_add(r, c, A.data_ptr(), B.data_ptr(), out.data_ptr(), int(bool(subtract)),
+                       _stream_ptr(stream)), "la_add")
     return out
 
 

@@ -57,6 +57,13 @@ static_assert(32 * NUM_CTRL_WARPS * CTRL_REGS + 32 * NUM_EPI_WARPS * EPI_REGS <=
 struct GemmArgs {
     float *C;
     int64_t n, p, ldc;  // C is n x p with row stride ldc
+    // Output addressing: element (r, c) of the n x p product goes to
+    //   C + r * ldc + c * cstride                      (r <  half_rows or half_rows == 0)
+    //   C + (r - half_rows) * ldc + half_off + c * cstride   (r >= half_rows)
+    // Real products use cstride 1, half_rows 0.  The complex embedding writes
+    // [Cr; Ci] into interleaved complex64 C: ldc = 2p, cstride 2, half_rows = n,
+    // half_off = 1.
+    int64_t cstride, half_rows, half_off;
     int32_t num_kb;     // K-blocks of BK
     int32_t kc;         // K-blocks per TMEM chunk (promotion interval); >= num_kb: no promotion
     int32_t tiles_m, tiles_n, group_m;
@@ -137,8 +144,14 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 
 // Write one 32 x 32 piece of C held as (thread = row, v[i] = column i) through
 // a per-warp XOR-swizzled smem transpose (conflict-free both ways), so each
-// store instruction writes 128 contiguous bytes of one C row.  Rows >= n and
-// columns >= p are skipped (ragged edges); offsets are 64-bit.
+// store instruction writes one contiguous run of a C row (128 B for real
+// products).  Rows >= n and columns >= p are skipped (ragged edges); offsets
+// are 64-bit.
+__device__ __forceinline__ float *row_ptr(const GemmArgs &args, int64_t r) {
+    if (args.half_rows > 0 && r >= args.half_rows) return args.C + (r - args.half_rows) * args.ldc + args.half_off;
+    return args.C + r * args.ldc;
+}
+
 __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, uint32_t lane, int64_t row0,
                                             int64_t col0, const uint32_t (&v)[32]) {
 #pragma unroll
@@ -147,12 +160,18 @@ __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, u
     const int64_t col = col0 + lane;
     const int64_t rem = args.n - row0;
     if (col < args.p && rem > 0) {
-        float *cp = args.C + row0 * args.ldc + col;
-        if (rem >= 32) {
+        const int rows = rem < 32 ? (int)rem : 32;
+        if (args.half_rows == 0 && args.cstride == 1) {
+            float *cp = args.C + row0 * args.ldc + col;
+            if (rows == 32) {
 #pragma unroll 4
-            for (int rr = 0; rr < 32; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
+                for (int rr = 0; rr < 32; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
+            } else {
+                for (int rr = 0; rr < rows; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
+            }
         } else {
-            for (int rr = 0; rr < (int)rem; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
+            for (int rr = 0; rr < rows; rr++)
+                row_ptr(args, row0 + rr)[col * args.cstride] = tbuf[rr * 32 + (lane ^ rr)];
         }
     }
     __syncwarp();

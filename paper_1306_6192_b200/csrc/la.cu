@@ -184,7 +184,7 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
 
 template <int CG, int BN, int STAGES, int PASSES>
 static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C,
-                             int64_t ldc, int max_sms, cudaStream_t st, int *launches) {
+                             int64_t ldc, int max_sms, cudaStream_t st, int *launches, const OutSpec &out) {
     using Cfg = GemmCfg<CG, BN, STAGES, PASSES>;
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     la_status s;
@@ -199,10 +199,13 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         tb_lo = tb_hi;
     }
     GemmArgs args;
-    args.C = C + j0;
+    args.C = C + j0 * out.cstride;
     args.n = n;
     args.p = pc;
     args.ldc = ldc;
+    args.cstride = out.cstride;
+    args.half_rows = out.half_rows;
+    args.half_off = out.half_off;
     args.num_kb = (int32_t)((m + BK - 1) / BK);
     // Promotion only in 3xTF32: plain TF32's 2^-9 bound is 2^11 times looser than
     // the truncation bias of whole-K accumulation (~3 x 2^-20 S at K = 16384).
@@ -301,14 +304,14 @@ static int choose_cta_group(int64_t n, int64_t pc) {
 }
 
 la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
-                   int max_sms, cudaStream_t st, int *launches) {
+                   int max_sms, cudaStream_t st, int *launches, OutSpec out) {
     const int cg = choose_cta_group(n, pc);
     if (ops.passes == 3) {
-        if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
-        return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+        if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
+        return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
     }
-    if (cg == 2) return launch_gemm<2, 256, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
-    return launch_gemm<1, 128, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches);
+    if (cg == 2) return launch_gemm<2, 256, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
+    return launch_gemm<1, 128, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
 }
 
 la_status validate_gemm(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const float *C) {
@@ -544,6 +547,105 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     LA_CK(cudaStreamSynchronize(g_state.d2h));
     LA_CK(cudaStreamSynchronize(st));
     return LA_OK;
+}
+
+// Complex single-precision product (Table 2 "Complex Float") through
+// the real embedding [[Ar, -Ai], [Ai, Ar]] . [Br; Bi] = [Cr; Ci] (split.cuh),
+// one persistent GEMM launch writing interleaved complex64 C.
+la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B, float *d_C,
+                   void *stream) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
+    if (2 * n > (int64_t)1 << 31 || 2 * m > (int64_t)1 << 31 || p > (int64_t)1 << 31)
+        return fail(LA_ERR_UNSUPPORTED, "dimension exceeds the int32 TMA coordinate range");
+    if (!d_A || !d_B || !d_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if ((reinterpret_cast<uintptr_t>(d_A) | reinterpret_cast<uintptr_t>(d_B)) & 7)
+        return fail(LA_ERR_INVALID_VALUE, "complex operands must be 8-byte aligned");
+    auto overlap = [](const void *x, int64_t xb, const void *y, int64_t yb) {
+        const char *a = (const char *)x, *b = (const char *)y;
+        return a < b + yb && b < a + xb;
+    };
+    if (overlap(d_C, 8 * n * p, d_A, 8 * n * m) || overlap(d_C, 8 * n * p, d_B, 8 * m * p))
+        return fail(LA_ERR_INVALID_VALUE, "C overlaps A or B");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
+    const int64_t n2 = 2 * n, m2 = 2 * m;
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&ws, operands_bytes(n2, m2, p, passes), g_state.pool, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LA_ERR_OUT_OF_MEMORY, "workspace");
+    }
+    const Operands ops = operands_carve(ws, n2, m2, p, passes);
+    int launches = 0;
+    la_status s = LA_OK;
+    {
+        cudaEvent_t t0;
+        if ((s = timing_begin(st, &t0)) != LA_OK) return s;
+        const int64_t width = ops.mp - m;
+        dim3 ga((unsigned)std::min<int64_t>((width + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
+        dim3 gb((unsigned)((p + 31) / 32), (unsigned)((width + 31) / 32));
+        if (gb.y > 65535) return fail(LA_ERR_UNSUPPORTED, "m too large for the split grid");
+        const float2 *a2 = reinterpret_cast<const float2 *>(d_A);
+        const float2 *b2 = reinterpret_cast<const float2 *>(d_B);
+        if (passes == 3) {
+            split_complex_a_kernel<3><<<ga, 256, 0, st>>>(a2, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            split_complex_b_kernel<3><<<gb, dim3(32, 8), 0, st>>>(b2, ops.b_hi, ops.b_lo, m, p, ops.mp);
+        } else {
+            split_complex_a_kernel<1><<<ga, 256, 0, st>>>(a2, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            split_complex_b_kernel<1><<<gb, dim3(32, 8), 0, st>>>(b2, ops.b_hi, ops.b_lo, m, p, ops.mp);
+        }
+        launches += 2;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "complex split launch", __FILE__, __LINE__);
+        if ((s = timing_end(st, t0, TIMED_SPLIT)) != LA_OK) return s;
+    }
+    OutSpec out;
+    out.cstride = 2;
+    out.half_rows = n;
+    out.half_off = 1;
+    s = gemm_run(n2, m2, 0, p, ops, d_C, 2 * p, (int)g_state.max_sms, st, &launches, out);
+    e = cudaFreeAsync(ws, st);
+    g_state.last_launches = launches;
+    if (s == LA_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);
+    return s;
+}
+
+// Matrix addition / subtraction: C = A + B (subtract = 0) or A - B.
+// C may be exactly A or B (in place) but must not partially overlap them.
+la_status la_add(int64_t rows, int64_t cols, const float *d_A, const float *d_B, float *d_C, int subtract,
+                 void *stream) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (rows <= 0 || cols <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
+    if (!d_A || !d_B || !d_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
+    const int64_t count = rows * cols, bytes = 4 * count;
+    auto partial = [&](const void *x) {
+        const char *a = (const char *)d_C, *b = (const char *)x;
+        return a != b && a < b + bytes && b < a + bytes;
+    };
+    if (partial(d_A) || partial(d_B)) return fail(LA_ERR_INVALID_VALUE, "C partially overlaps A or B");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool vec = count % 4 == 0 &&
+                     ((reinterpret_cast<uintptr_t>(d_A) | reinterpret_cast<uintptr_t>(d_B) |
+                       reinterpret_cast<uintptr_t>(d_C)) & 15) == 0;
+    const int64_t items = vec ? count / 4 : count;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)g_state.sms * 8));
+    cudaEvent_t t0;
+    la_status s = timing_begin(st, &t0);
+    if (s != LA_OK) return s;
+    if (vec) {
+        const float4 *a = reinterpret_cast<const float4 *>(d_A), *b = reinterpret_cast<const float4 *>(d_B);
+        float4 *c = reinterpret_cast<float4 *>(d_C);
+        if (subtract) elementwise_vec4_kernel<true><<<blocks, 256, 0, st>>>(a, b, c, items);
+        else elementwise_vec4_kernel<false><<<blocks, 256, 0, st>>>(a, b, c, items);
+    } else {
+        if (subtract) elementwise_kernel<true><<<blocks, 256, 0, st>>>(d_A, d_B, d_C, items);
+        else elementwise_kernel<false><<<blocks, 256, 0, st>>>(d_A, d_B, d_C, items);
+    }
+    g_state.last_launches = 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "elementwise launch", __FILE__, __LINE__);
+    return timing_end(st, t0, TIMED_SPLIT);
 }
 
 la_status la_shard_rows(int64_t n, int rank, int ngpu, int64_t *row0, int64_t *rows) {

@@ -63,10 +63,15 @@ la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cud
 // m x (>= pc) row-major matrix with row stride ldb
 la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb, const Operands &ops,
                   cudaStream_t st, int *launches);
+// Output addressing beyond plain row-major (see GemmArgs in gemm_sm100.cuh).
+struct OutSpec {
+    int64_t cstride = 1, half_rows = 0, half_off = 0;
+};
+
 // C[:, j0:j0+pc] (n x pc block of a row-major matrix with row stride ldc) =
 // A . B[:, j0:j0+pc] from split operands; at most max_sms SMs (0 = all).
 la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
-                   int max_sms, cudaStream_t st, int *launches);
+                   int max_sms, cudaStream_t st, int *launches, OutSpec out = OutSpec());
 
 la_status comm_destroy();
 

@@ -94,3 +94,102 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
 }
 
 }  // namespace la
+
+namespace la {
+
+// ---- complex64 operands (Table 2 "Complex Float") ----------------
+// C = A.B with A (n x m), B (m x p) complex64, interleaved (re, im).  Computed as
+// one real product of the embedding
+//     [ Ar  -Ai ]   [ Br ]   [ Cr ]
+//     [ Ai   Ar ] . [ Bi ] = [ Ci ]        (2n x 2m) . (2m x p) = (2n x p)
+// which is four real GEMMs of work; every real and imaginary output component is
+// a 2m-term real inner product, so the 3xTF32 bound applies with the scales
+// sum |ar||br| + |ai||bi| (real) and sum |ar||bi| + |ai||br| (imaginary).
+// The split kernels write the embedding's hi/lo directly (Kp = pad4(2m) columns;
+// padding columns hold 0).
+
+// A (n x m complex) -> rows i and n+i of the 2n x Kp embedding.  One thread per
+// (row i, column k), k in [0, Kp - m): k < m writes (ar, -ai) into row i and
+// (ai, ar) into row n+i at columns k and m+k; k >= m zero-fills column m+k.
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_complex_a_kernel(const float2 *__restrict__ a, float *__restrict__ hi,
+                                                              float *__restrict__ lo, int64_t n, int64_t m,
+                                                              int64_t kp) {
+    const int64_t width = kp - m;
+    for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
+        for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < width;
+             k += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t top = r * kp, bot = (n + r) * kp;
+            if (k < m) {
+                const float2 v = a[r * m + k];
+                split_store<PASSES>(v.x, hi, lo, top + k);
+                split_store<PASSES>(-v.y, hi, lo, top + m + k);
+                split_store<PASSES>(v.y, hi, lo, bot + k);
+                split_store<PASSES>(v.x, hi, lo, bot + m + k);
+            } else {
+                split_store<PASSES>(0.0f, hi, lo, top + m + k);
+                split_store<PASSES>(0.0f, hi, lo, bot + m + k);
+            }
+        }
+    }
+}
+
+// B (m x p complex) -> Bt (p x Kp): Bt[j][k] = Br[k][j], Bt[j][m + k] = Bi[k][j],
+// columns [2m, Kp) zero.  32x32 complex tiles through smem; block (32, 8).
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_complex_b_kernel(const float2 *__restrict__ b, float *__restrict__ hi,
+                                                              float *__restrict__ lo, int64_t m, int64_t p,
+                                                              int64_t kp) {
+    __shared__ float2 tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t j0 = (int64_t)blockIdx.x * 32;
+    const int64_t k0 = (int64_t)blockIdx.y * 32;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t k = k0 + ty + 8 * i, j = j0 + tx;
+        tile[ty + 8 * i][tx] = (k < m && j < p) ? b[k * p + j] : make_float2(0.0f, 0.0f);
+    }
+    __syncthreads();
+    const int64_t width = kp - m;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t j = j0 + ty + 8 * i, k = k0 + tx;
+        if (j >= p || k >= width) continue;
+        const float2 v = tile[tx][ty + 8 * i];
+        if (k < m) {
+            split_store<PASSES>(v.x, hi, lo, j * kp + k);
+            split_store<PASSES>(v.y, hi, lo, j * kp + m + k);
+        } else {
+            split_store<PASSES>(0.0f, hi, lo, j * kp + m + k);
+        }
+    }
+}
+
+// ---- matrix addition / subtraction -----------------------------------
+// C = A + B or A - B elementwise, one binary32 operation per element (exact IEEE
+// RN: bitwise equal to any correct implementation).  HBM-bound: 12 B/element.
+template <bool SUB>
+__global__ void __launch_bounds__(256) elementwise_vec4_kernel(const float4 *__restrict__ a,
+                                                               const float4 *__restrict__ b,
+                                                               float4 *__restrict__ c, int64_t count4) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = __ldcs(a + i), y = __ldcs(b + i);
+        float4 z;
+        z.x = SUB ? x.x - y.x : x.x + y.x;
+        z.y = SUB ? x.y - y.y : x.y + y.y;
+        z.z = SUB ? x.z - y.z : x.z + y.z;
+        z.w = SUB ? x.w - y.w : x.w + y.w;
+        __stcs(c + i, z);
+    }
+}
+
+template <bool SUB>
+__global__ void __launch_bounds__(256) elementwise_kernel(const float *__restrict__ a, const float *__restrict__ b,
+                                                          float *__restrict__ c, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c[i] = SUB ? a[i] - b[i] : a[i] + b[i];
+}
+
+}  // namespace la
