@@ -236,3 +236,24 @@ def test_config4_16384_sampled(la, kind):
 
 def test_config4_16384_integer_freivalds(la):
     _sampled_check(la, 16384, 16384, 16384, "integer", freivalds=True)
+
+
+def test_n65536_indexing_sampled(la):
+    """Config C5's size on one GPU: 64-bit offsets everywhere (n*p = 2^32 would
+    overflow Listing 4's 32-bit `int c`).  Integer inputs, sampled rows
+    and columns at the corners and the 2^31-element boundary, exact."""
+    n = 65536
+    free, _ = torch.cuda.mem_get_info()
+    if free < 130 * 2 ** 30:
+        pytest.skip("needs ~120 GiB of device memory")
+    A, B = inputs.pair(n, n, n, "integer", device="cuda")
+    C = la.gemm(A, B)
+    torch.cuda.synchronize()
+    rows = [0, 1, 32767, 32768, n - 2, n - 1]
+    cols = [0, 1, 32767, 32768, n - 2, n - 1]
+    As = inputs.generate(n, n, 0, "integer", row_idx=rows).numpy()
+    Bs = inputs.generate(n, n, 1, "integer", col_idx=cols).numpy()
+    got = C[rows][:, cols].cpu().numpy()
+    del A, B, C
+    torch.cuda.empty_cache()
+    _check(As, Bs, got, "integer", "3xtf32")
