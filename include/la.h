@@ -132,6 +132,16 @@ LA_API la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A,
 LA_API la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B,
                           float *d_C, void *stream);
 
+/* Double-precision product (Table 2 "Double" column; 8-byte tiles,
+ * P:130): d_A n x m, d_B m x p, d_C n x p, row-major binary64, device, 8-byte
+ * aligned.  FP64 tensor path (DMMA, mma.sync f64): every product and sum is a
+ * binary64 operation (fused multiply-add), so |C - C_ref| <= 2 gamma_m S with
+ * S = sum_r |a_ir||b_rj|, gamma_m = m 2^-53 / (1 - m 2^-53), against the binary64
+ * Listing 1; integer-valued inputs with partial sums below 2^53 are exact.
+ * Errors: NOT_INITIALIZED, INVALID_VALUE, UNSUPPORTED, CUDA. */
+LA_API la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const double *d_B,
+                          double *d_C, void *stream);
+
 /* Matrix addition / subtraction (PAPER.md section "Rezultaty i wnioski", P:203:
  * "Dodawanie macierzy ... 16 777 216 operacji elementarnych" at 4096 x 4096):
  * C = A + B (subtract = 0) or C = A - B (subtract != 0), rows x cols row-major

@@ -32,6 +32,7 @@ SEED = 13066192
 SEED_REPEAT = 13066193
 ID_A, ID_B = 0, 1
 MODES = ("random", "stress", "integer")
+MODES_F64 = ("f64", "integer")
 GRID_SHIFT = {"random": 23, "stress": 24, "integer": 0}
 
 _M64 = (1 << 64) - 1
@@ -117,6 +118,38 @@ def generate(rows: int, cols: int, matrix_id: int, mode: str = "random",
         rr = r[r0:r0 + rows_per]
         idx = rr[:, None] * cols + c[None, :]
         out[r0:r0 + rr.numel()] = _values(idx, key, mode)
+    return out
+
+
+def value_int_f64(seed: int, matrix_id: int, idx: int) -> float:
+    """Pure-Python reference for one binary64 element (tests only)."""
+    h = splitmix64_int(splitmix64_int((seed ^ matrix_id) & _M64) ^ idx)
+    return ((h >> 11) - (1 << 52)) * 2.0 ** -52
+
+
+def generate_f64(rows: int, cols: int, matrix_id: int, mode: str = "f64", seed: int = SEED, device="cpu",
+                 row_idx=None, col_idx=None, chunk: int = 1 << 23) -> torch.Tensor:
+    """Binary64 inputs for the double-precision product: mode "f64" draws
+    ((h >> 11) - 2^52) * 2^-52 (53-bit significands, uniform on the 2^-52 grid in
+    [-1, 1)); mode "integer" is the integer mode above, as float64."""
+    device = torch.device(device)
+    key = _key(seed, matrix_id)
+    r = (torch.arange(rows, dtype=torch.int64, device=device) if row_idx is None
+         else torch.as_tensor(row_idx, dtype=torch.int64, device=device))
+    c = (torch.arange(cols, dtype=torch.int64, device=device) if col_idx is None
+         else torch.as_tensor(col_idx, dtype=torch.int64, device=device))
+    out = torch.empty((r.numel(), c.numel()), dtype=torch.float64, device=device)
+    if out.numel() == 0:
+        return out
+    rows_per = max(1, chunk // max(1, c.numel()))
+    for r0 in range(0, r.numel(), rows_per):
+        rr = r[r0:r0 + rows_per]
+        idx = rr[:, None] * cols + c[None, :]
+        if mode == "f64":
+            h = _splitmix64(idx ^ key)
+            out[r0:r0 + rr.numel()] = (_lsr(h, 11) - (1 << 52)).to(torch.float64) * 2.0 ** -52
+        else:
+            out[r0:r0 + rr.numel()] = _values(idx, key, mode).to(torch.float64)
     return out
 
 

@@ -23,6 +23,8 @@ freivalds(A, B, C, x)          exact int64 Freivalds check C.x == A.(B.x).
 elementwise(A, B, subtract)    C = A + B or A - B, one binary32 op per element.
 cgemm(A, B)                    complex64 Listing 1 (Table 2 "Complex Float").
 cabs_scale(A, B)               complex tolerance scales (real part, imaginary part).
+dgemm(A, B)                    binary64 Listing 1 (Table 2 "Double").
+dabs_scale(A, B)               binary64 tolerance scale for dgemm.
 """
 from __future__ import annotations
 
@@ -71,6 +73,10 @@ def _load():
         lib.oracle_cgemm.restype = ctypes.c_int
         lib.oracle_cabs_scale.argtypes = [i64, i64, i64, fp, fp, dp]
         lib.oracle_cabs_scale.restype = ctypes.c_int
+        lib.oracle_dgemm.argtypes = [i64, i64, i64, fp, fp, fp]
+        lib.oracle_dgemm.restype = ctypes.c_int
+        lib.oracle_dabs_scale.argtypes = [i64, i64, i64, fp, fp, dp]
+        lib.oracle_dabs_scale.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -187,3 +193,27 @@ def cabs_scale(A, B):
     S = np.empty((n, p, 2), dtype=np.float64)
     _load().oracle_cabs_scale(n, m, p, _ptr(A), _ptr(B), _ptr(S))
     return S[..., 0], S[..., 1]
+
+
+def _f64(x) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x), dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    return a
+
+
+def dgemm(A, B) -> np.ndarray:
+    """Binary64 Listing 1: C = A.B (mul then add, ascending r, no FMA)."""
+    A, B = _f64(A), _f64(B)
+    n, m, p = _dims(A, B)
+    C = np.empty((n, p), dtype=np.float64)
+    _load().oracle_dgemm(n, m, p, _ptr(A), _ptr(B), _ptr(C))
+    return C
+
+
+def dabs_scale(A, B) -> np.ndarray:
+    A, B = _f64(A), _f64(B)
+    n, m, p = _dims(A, B)
+    S = np.empty((n, p), dtype=np.float64)
+    _load().oracle_dabs_scale(n, m, p, _ptr(A), _ptr(B), _ptr(S))
+    return S

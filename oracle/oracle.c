@@ -277,3 +277,33 @@ int oracle_cabs_scale(int64_t n, int64_t m, int64_t p, const float *A, const flo
         }
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Double-precision Listing 1 (Table 2 "Double" column): binary64  */
+/* arrays and accumulator, product then sum each RN-even, no FMA, ascending r. */
+/* ------------------------------------------------------------------------- */
+int oracle_dgemm(int64_t n, int64_t m, int64_t p, const double *A, const double *B, double *C)
+{
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t j = 0; j < p; j++) {
+            double s = 0.0;
+            for (int64_t k = 0; k < m; k++) {
+                double t = A[i * m + k] * B[k * p + j];
+                s = s + t;
+            }
+            C[i * p + j] = s;
+        }
+    return 0;
+}
+
+/* S_ij = sum_r |a_ir||b_rj| for binary64 inputs, accumulated in binary64. */
+int oracle_dabs_scale(int64_t n, int64_t m, int64_t p, const double *A, const double *B, double *S)
+{
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t j = 0; j < p; j++) {
+            double s = 0.0;
+            for (int64_t k = 0; k < m; k++) s += fabs(A[i * m + k]) * fabs(B[k * p + j]);
+            S[i * p + j] = s;
+        }
+    return 0;
+}

@@ -29,7 +29,7 @@ OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3}
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
            "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times", "la_cgemm",
-           "la_add")
+           "la_add", "la_dgemm")
 
 
 class LaError(RuntimeError):
@@ -51,6 +51,7 @@ def _load() -> ctypes.CDLL:
         "la_gemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_gemm_host": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_cgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_dgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_add": ([i64, i64, vp, vp, vp, ctypes.c_int, vp], st),
         "la_get_unique_id": ([vp], st),
         "la_comm_init": ([vp, ctypes.c_int, ctypes.c_int], st),
@@ -171,6 +172,24 @@ def cgemm(A, B, out=None, stream=None):
     if out is None:
         out = torch.empty((n, p), dtype=torch.complex64, device=A.device)
     _check(_lib.la_cgemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_cgemm")
+    return out
+
+
+def dgemm(A, B, out=None, stream=None):
+    """C = A . B for float64 CUDA tensors (la_dgemm, Table 2 "Double")."""
+    import torch
+    for t, nm in ((A, "A"), (B, "B")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+            raise TypeError(f"{nm} must be a float64 CUDA tensor")
+        if t.dim() != 2 or not t.is_contiguous():
+            raise ValueError(f"{nm} must be a contiguous 2-D (row-major) matrix")
+    n, m = A.shape
+    m2, p = B.shape
+    if m != m2:
+        raise ValueError("inner dimension mismatch")
+    if out is None:
+        out = torch.empty((n, p), dtype=torch.float64, device=A.device)
+    _check(_lib.la_dgemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_dgemm")
     return out
 
 

@@ -1,0 +1,147 @@
+// dgemm_sm100.cuh -- double-precision C = A . B (Table 2 "Double" column,
+// PAPER.md P:222-228; 8-byte shared-memory tiles).
+//
+// tcgen05 has no f64 kind; the B200's FP64 tensor path is DMMA (SASS
+// DMMA.8x8x4, reached through mma.sync m16n8k8 f64, which ptxas splits into four
+// DMMA.8x8x4).  The kernel is Listing 4's structure widened:
+//   * 128 x 128 block tiles, 8 warps of 64 x 32 (4 x 4 m16n8 fragments each);
+//   * K staged 16 doubles at a time in a 3-stage cp.async ring (8-byte copies,
+//     zero-filled outside the matrix, so any n, m, p >= 1 works), padded rows
+//     (A: 20 doubles, B: 132) so every fragment load is bank-conflict free;
+//   * fp64 FMA accumulation in registers (64 doubles per thread), each C element
+//     written once, 64-bit offsets.
+// Numerics: every product and sum is an IEEE binary64 operation (fused
+// multiply-add), so |C - C_ref| <= 2 gamma_m(2^-53) sum|a||b| against the
+// binary64 oracle, and integer inputs are exact.
+#pragma once
+#include <cstdint>
+
+namespace la {
+
+constexpr int DBM = 128, DBN = 128, DBK = 16, DSTAGES = 3;
+constexpr int DLDA = DBK + 4;  // doubles per A row in smem (160 B: conflict-free fragment loads)
+constexpr int DLDB = DBN + 4;  // doubles per B row in smem (1056 B)
+constexpr int DTHREADS = 256;
+constexpr int DSMEM_BYTES = DSTAGES * (DBM * DLDA + DBK * DLDB) * 8;
+
+__device__ __forceinline__ void cp_async_f64(void *dst, const double *src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 8 : 0;  // src-size 0: zero-fill, no global read
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+__global__ void __launch_bounds__(DTHREADS, 1)
+    dgemm_sm100_kernel(const double *__restrict__ A, const double *__restrict__ B, double *__restrict__ C,
+                       int64_t n, int64_t m, int64_t p) {
+    extern __shared__ __align__(16) double dsm[];
+    double *As = dsm;                              // [DSTAGES][DBM][DLDA]
+    double *Bs = dsm + DSTAGES * DBM * DLDA;       // [DSTAGES][DBK][DLDB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;         // fragment row group / thread in group
+    const int wm = warp >> 2, wn = warp & 3;       // warp tile origin: rows wm*64, cols wn*32
+    const int64_t m0 = (int64_t)blockIdx.y * DBM, n0 = (int64_t)blockIdx.x * DBN;
+    const int kt_count = (int)((m + DBK - 1) / DBK);
+
+    auto load_stage = [&](int stage, int kt) {
+        const int64_t k0 = (int64_t)kt * DBK;
+        double *as = As + stage * DBM * DLDA;
+        double *bs = Bs + stage * DBK * DLDB;
+#pragma unroll
+        for (int i = 0; i < DBM * DBK / DTHREADS; i++) {  // A: 128 rows x 16
+            const int idx = tid + i * DTHREADS, r = idx / DBK, c = idx % DBK;
+            const int64_t gr = m0 + r, gc = k0 + c;
+            const bool ok = gr < n && gc < m;
+            cp_async_f64(as + r * DLDA + c, ok ? A + gr * m + gc : A, ok);
+        }
+#pragma unroll
+        for (int i = 0; i < DBK * DBN / DTHREADS; i++) {  // B: 16 rows x 128
+            const int idx = tid + i * DTHREADS, r = idx / DBN, c = idx % DBN;
+            const int64_t gr = k0 + r, gc = n0 + c;
+            const bool ok = gr < m && gc < p;
+            cp_async_f64(bs + r * DLDB + c, ok ? B + gr * p + gc : B, ok);
+        }
+    };
+
+    double acc[4][4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int v = 0; v < 4; v++) acc[i][j][v] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < DSTAGES - 1; s++) {
+        if (s < kt_count) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < kt_count; kt++) {
+        cp_async_wait<DSTAGES - 2>();
+        __syncthreads();  // stage kt landed for everyone; stage kt-1 no longer read
+        const int nxt = kt + DSTAGES - 1;
+        if (nxt < kt_count) load_stage(nxt % DSTAGES, nxt);
+        cp_async_commit();
+        const double *as = As + (kt % DSTAGES) * DBM * DLDA + (wm * 64) * DLDA;
+        const double *bs = Bs + (kt % DSTAGES) * DBK * DLDB + wn * 32;
+#pragma unroll
+        for (int kk = 0; kk < DBK; kk += 8) {
+            double af[4][4], bf[4][2];
+#pragma unroll
+            for (int mi = 0; mi < 4; mi++) {
+                const double *a = as + (mi * 16 + g) * DLDA + kk + t;
+                af[mi][0] = a[0];
+                af[mi][1] = a[8 * DLDA];
+                af[mi][2] = a[4];
+                af[mi][3] = a[8 * DLDA + 4];
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ni++) {
+                const double *b = bs + (kk + t) * DLDB + ni * 8 + g;
+                bf[ni][0] = b[0];
+                bf[ni][1] = b[4 * DLDB];
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+                for (int ni = 0; ni < 4; ni++) dmma_16x8x8(acc[mi][ni], af[mi], bf[ni]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // write-back: d0 (g, 2t), d1 (g, 2t+1), d2 (g+8, 2t), d3 (g+8, 2t+1)
+    const bool pair_ok = (p & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+            const int64_t row = m0 + wm * 64 + mi * 16 + g + 8 * half;
+            if (row >= n) continue;
+            double *crow = C + row * p;
+#pragma unroll
+            for (int ni = 0; ni < 4; ni++) {
+                const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t;
+                const double v0 = acc[mi][ni][2 * half], v1 = acc[mi][ni][2 * half + 1];
+                if (pair_ok && col + 1 < p) {
+                    *reinterpret_cast<double2 *>(crow + col) = make_double2(v0, v1);
+                } else {
+                    if (col < p) crow[col] = v0;
+                    if (col + 1 < p) crow[col + 1] = v1;
+                }
+            }
+        }
+}
+
+}  // namespace la

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "dgemm_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "la.h"
 #include "la_internal.h"
@@ -609,6 +610,40 @@ la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const floa
     g_state.last_launches = launches;
     if (s == LA_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);
     return s;
+}
+
+// Double-precision product (Table 2 "Double" column) on the DMMA path.
+la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const double *d_B, double *d_C,
+                   void *stream) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
+    if (!d_A || !d_B || !d_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if ((reinterpret_cast<uintptr_t>(d_A) | reinterpret_cast<uintptr_t>(d_B) | reinterpret_cast<uintptr_t>(d_C)) & 7)
+        return fail(LA_ERR_INVALID_VALUE, "double operands must be 8-byte aligned");
+    auto overlap = [](const void *x, int64_t xb, const void *y, int64_t yb) {
+        const char *a = (const char *)x, *b = (const char *)y;
+        return a < b + yb && b < a + xb;
+    };
+    if (overlap(d_C, 8 * n * p, d_A, 8 * n * m) || overlap(d_C, 8 * n * p, d_B, 8 * m * p))
+        return fail(LA_ERR_INVALID_VALUE, "C overlaps A or B");
+    const int64_t gy = (n + DBM - 1) / DBM, gx = (p + DBN - 1) / DBN;
+    if (gy > 65535 || gx > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "matrix too large for the DGEMM grid");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(dgemm_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             DSMEM_BYTES);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(dgemm)", __FILE__, __LINE__);
+        attr = true;
+    }
+    cudaEvent_t t0;
+    la_status s = timing_begin(st, &t0);
+    if (s != LA_OK) return s;
+    dgemm_sm100_kernel<<<dim3((unsigned)gx, (unsigned)gy), DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
+    g_state.last_launches = 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "dgemm launch", __FILE__, __LINE__);
+    return timing_end(st, t0, TIMED_GEMM);
 }
 
 // Matrix addition / subtraction: C = A + B (subtract = 0) or A - B.

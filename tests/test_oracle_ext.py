@@ -106,3 +106,48 @@ def test_complex_error_vs_exact(mode, shift):
     assert np.all(np.abs(C.real - er) <= g * Sr)
     assert np.all(np.abs(C.imag - ei) <= g * Si)
     assert np.max(np.abs(C.real - er) / Sr) <= 2.0 ** -21
+
+
+# ------------------------------------------------------------------ double
+def test_dgemm_integer_bruteforce():
+    rng = np.random.default_rng(21)
+    for n in range(1, 7):
+        for m in range(1, 7):
+            for p in range(1, 7):
+                A = rng.integers(-(2 ** 20), 2 ** 20, (n, m))
+                B = rng.integers(-(2 ** 20), 2 ** 20, (m, p))
+                C = oracle.dgemm(A.astype(np.float64), B.astype(np.float64))
+                assert np.array_equal(C.astype(np.int64), A @ B), (n, m, p)
+
+
+def test_dgemm_binary64_ascending_semantics():
+    A = inputs.generate_f64(5, 900, 0).numpy()
+    B = inputs.generate_f64(900, 4, 1).numpy()
+    C = oracle.dgemm(A, B)
+    for i in range(5):
+        for j in range(4):
+            ref = np.cumsum(np.multiply(A[i], B[:, j]))[-1]
+            assert C[i, j] == ref
+
+
+def test_dgemm_error_vs_exact_python_integers():
+    m = 300
+    A = inputs.generate_f64(4, m, 0).numpy()
+    B = inputs.generate_f64(m, 3, 1).numpy()
+    C = oracle.dgemm(A, B)
+    S = oracle.dabs_scale(A, B)
+    ka = [[int(round(x * 2 ** 52)) for x in row] for row in A]
+    kb = [[int(round(x * 2 ** 52)) for x in row] for row in B]
+    u = 2.0 ** -53
+    g = m * u / (1 - m * u)
+    from fractions import Fraction
+    for i in range(4):
+        for j in range(3):
+            exact = Fraction(sum(ka[i][r] * kb[r][j] for r in range(m)), 2 ** 104)
+            assert abs(Fraction(C[i, j]) - exact) <= Fraction(g) * Fraction(S[i, j])
+
+
+def test_dgemm_generator_matches_python():
+    idx = [0, 7, 99999, 2 ** 33 + 1]
+    t = inputs.generate_f64(1, 2 ** 35, 1, col_idx=idx)
+    assert t.flatten().tolist() == [inputs.value_int_f64(inputs.SEED, 1, i) for i in idx]

@@ -95,3 +95,43 @@ def test_cgemm_real_inputs_match_la_gemm_bitwise(la):
     R = la.gemm(A, B)
     assert torch.equal(C.real.contiguous(), R)
     assert not C.imag.any()
+
+
+def _dcheck(A, B, C, kind):
+    An, Bn = A.cpu().numpy(), B.cpu().numpy()
+    ref = oracle.dgemm(An, Bn)
+    if kind == "integer":
+        assert np.array_equal(C, ref)
+        return
+    S = oracle.dabs_scale(An, Bn)
+    m = An.shape[1]
+    u = 2.0 ** -53
+    g = m * u / (1 - m * u)
+    ratio = (np.abs(C - ref) / np.maximum(S, 1e-300)).max()
+    assert ratio <= 2 * g, f"{ratio / g:.3f} x gamma_m"
+
+
+@pytest.mark.parametrize("kind", ["integer", "f64"])
+@pytest.mark.parametrize("n,m,p", [(1, 1, 1), (5, 3, 7), (128, 16, 128), (129, 17, 131), (300, 1000, 257),
+                                   (1024, 1024, 1024)])
+def test_dgemm_parity(la, kind, n, m, p):
+    A = inputs.generate_f64(n, m, 0, kind)
+    B = inputs.generate_f64(m, p, 1, kind)
+    C = la.dgemm(A.cuda(), B.cuda()).cpu().numpy()
+    _dcheck(A, B, C, kind)
+
+
+def test_dgemm_4096_sampled(la):
+    n = 4096
+    A = inputs.generate_f64(n, n, 0, device="cuda")
+    B = inputs.generate_f64(n, n, 1, device="cuda")
+    C = la.dgemm(A, B)
+    rows, cols = [0, 127, 128, 2047, 4095], [0, 1, 128, 3000, 4095]
+    _dcheck(A[rows].cpu(), B[:, cols].cpu(), C[rows][:, cols].cpu().numpy(), "f64")
+
+
+def test_dgemm_odd_ldc_unaligned_pairs(la):
+    """p odd: the epilogue's paired (16-byte) stores must fall back to scalars."""
+    A = inputs.generate_f64(70, 33, 0, "integer").cuda()
+    B = inputs.generate_f64(33, 45, 1, "integer").cuda()
+    _dcheck(A.cpu(), B.cpu(), la.dgemm(A, B).cpu().numpy(), "integer")
