@@ -5,9 +5,10 @@
 // DMMA.8x8x4, reached through mma.sync m16n8k8 f64, which ptxas splits into four
 // DMMA.8x8x4).  The kernel is Listing 4's structure widened:
 //   * 128 x 128 block tiles, 8 warps of 64 x 32 (4 x 4 m16n8 fragments each);
-//   * K staged 16 doubles at a time in a 3-stage cp.async ring (8-byte copies,
-//     zero-filled outside the matrix, so any n, m, p >= 1 works), padded rows
-//     (A: 20 doubles, B: 132) so every fragment load is bank-conflict free;
+//   * K staged 32 doubles at a time in a 3-stage cp.async ring (16-byte copies
+//     when m, p are even and A, B 16-byte aligned, else 8-byte; zero-filled
+//     outside the matrix, so any n, m, p >= 1 works), padded rows (A: 36
+//     doubles, B: 132) so every fragment load is bank-conflict free;
 //   * fp64 FMA accumulation in registers (64 doubles per thread), each C element
 //     written once, 64-bit offsets.
 // Numerics: every product and sum is an IEEE binary64 operation (fused
@@ -18,8 +19,8 @@
 
 namespace la {
 
-constexpr int DBM = 128, DBN = 128, DBK = 16, DSTAGES = 3;
-constexpr int DLDA = DBK + 4;  // doubles per A row in smem (160 B: conflict-free fragment loads)
+constexpr int DBM = 128, DBN = 128, DBK = 32, DSTAGES = 3;
+constexpr int DLDA = DBK + 4;  // doubles per A row in smem (288 B: conflict-free fragment loads)
 constexpr int DLDB = DBN + 4;  // doubles per B row in smem (1056 B)
 constexpr int DTHREADS = 256;
 constexpr int DSMEM_BYTES = DSTAGES * (DBM * DLDA + DBK * DLDB) * 8;
@@ -28,6 +29,11 @@ __device__ __forceinline__ void cp_async_f64(void *dst, const double *src, bool 
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     const int sz = valid ? 8 : 0;  // src-size 0: zero-fill, no global read
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_f64x2(void *dst, const double *src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -43,6 +49,8 @@ __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4]
         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
+// VEC16: m and p even and A, B 16-byte aligned -> 16-byte copies (two doubles).
+template <bool VEC16>
 __global__ void __launch_bounds__(DTHREADS, 1)
     dgemm_sm100_kernel(const double *__restrict__ A, const double *__restrict__ B, double *__restrict__ C,
                        int64_t n, int64_t m, int64_t p) {
@@ -59,19 +67,36 @@ __global__ void __launch_bounds__(DTHREADS, 1)
         const int64_t k0 = (int64_t)kt * DBK;
         double *as = As + stage * DBM * DLDA;
         double *bs = Bs + stage * DBK * DLDB;
+        if constexpr (VEC16) {
 #pragma unroll
-        for (int i = 0; i < DBM * DBK / DTHREADS; i++) {  // A: 128 rows x 16
-            const int idx = tid + i * DTHREADS, r = idx / DBK, c = idx % DBK;
-            const int64_t gr = m0 + r, gc = k0 + c;
-            const bool ok = gr < n && gc < m;
-            cp_async_f64(as + r * DLDA + c, ok ? A + gr * m + gc : A, ok);
-        }
+            for (int i = 0; i < DBM * DBK / 2 / DTHREADS; i++) {  // A: 128 rows x 16 pairs
+                const int idx = tid + i * DTHREADS, r = idx / (DBK / 2), c = 2 * (idx % (DBK / 2));
+                const int64_t gr = m0 + r, gc = k0 + c;
+                const bool ok = gr < n && gc < m;
+                cp_async_f64x2(as + r * DLDA + c, ok ? A + gr * m + gc : A, ok);
+            }
 #pragma unroll
-        for (int i = 0; i < DBK * DBN / DTHREADS; i++) {  // B: 16 rows x 128
-            const int idx = tid + i * DTHREADS, r = idx / DBN, c = idx % DBN;
-            const int64_t gr = k0 + r, gc = n0 + c;
-            const bool ok = gr < m && gc < p;
-            cp_async_f64(bs + r * DLDB + c, ok ? B + gr * p + gc : B, ok);
+            for (int i = 0; i < DBK * DBN / 2 / DTHREADS; i++) {  // B: 32 rows x 64 pairs
+                const int idx = tid + i * DTHREADS, r = idx / (DBN / 2), c = 2 * (idx % (DBN / 2));
+                const int64_t gr = k0 + r, gc = n0 + c;
+                const bool ok = gr < m && gc < p;
+                cp_async_f64x2(bs + r * DLDB + c, ok ? B + gr * p + gc : B, ok);
+            }
+        } else {
+#pragma unroll 4
+            for (int i = 0; i < DBM * DBK / DTHREADS; i++) {  // A: 128 rows x 32
+                const int idx = tid + i * DTHREADS, r = idx / DBK, c = idx % DBK;
+                const int64_t gr = m0 + r, gc = k0 + c;
+                const bool ok = gr < n && gc < m;
+                cp_async_f64(as + r * DLDA + c, ok ? A + gr * m + gc : A, ok);
+            }
+#pragma unroll 4
+            for (int i = 0; i < DBK * DBN / DTHREADS; i++) {  // B: 32 rows x 128
+                const int idx = tid + i * DTHREADS, r = idx / DBN, c = idx % DBN;
+                const int64_t gr = k0 + r, gc = n0 + c;
+                const bool ok = gr < m && gc < p;
+                cp_async_f64(bs + r * DLDB + c, ok ? B + gr * p + gc : B, ok);
+            }
         }
     };
 

@@ -631,15 +631,22 @@ la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const dou
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dgemm_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(dgemm_sm100_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              DSMEM_BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dgemm_sm100_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     DSMEM_BYTES);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(dgemm)", __FILE__, __LINE__);
         attr = true;
     }
+    const bool vec16 = m % 2 == 0 && p % 2 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(d_A) | reinterpret_cast<uintptr_t>(d_B)) & 15) == 0;
     cudaEvent_t t0;
     la_status s = timing_begin(st, &t0);
     if (s != LA_OK) return s;
-    dgemm_sm100_kernel<<<dim3((unsigned)gx, (unsigned)gy), DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
+    const dim3 grid((unsigned)gx, (unsigned)gy);
+    if (vec16) dgemm_sm100_kernel<true><<<grid, DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
+    else dgemm_sm100_kernel<false><<<grid, DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
     g_state.last_launches = 1;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "dgemm launch", __FILE__, __LINE__);

@@ -74,5 +74,32 @@ def main():
               flush=True)
 
 
+def dgemm_rows():
+    la.init(0)
+    for n in (4096, 8192):
+        A = inputs.generate_f64(n, n, 0, device="cuda")
+        B = inputs.generate_f64(n, n, 1, device="cuda")
+        C = torch.empty_like(A)
+        ms = timed(lambda: la.dgemm(A, B, out=C), 10 if n <= 4096 else 5)
+        tf = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+        msc = timed(lambda: torch.matmul(A, B, out=C), 10 if n <= 4096 else 5)
+        tfc = 2.0 * n ** 3 / (msc * 1e-3) / 1e12
+        rows = list(np.linspace(0, n - 1, 8).astype(int))
+        cols = list(np.linspace(0, n - 1, 8).astype(int))
+        C2 = la.dgemm(A, B)
+        As, Bs = A[rows].cpu().numpy(), B[:, cols].cpu().numpy()
+        t0 = time.perf_counter()
+        ref = oracle.dgemm(As, Bs)
+        to = (time.perf_counter() - t0) * n * n / 64
+        S = oracle.dabs_scale(As, Bs)
+        err = (np.abs(C2[rows][:, cols].cpu().numpy() - ref) / S).max() / 2.0 ** -53
+        print(f"| dgemm (DMMA) | {n}x{n} | {ms:.2f} | {tf:.1f} TFLOP/s | 40 TFLOP/s FP64 datasheet; cuBLAS DGEMM "
+              f"{tfc:.1f} TFLOP/s ({msc:.2f} ms) on this box | {tf / 40:.2f} of datasheet, {tf / tfc:.2f} of cuBLAS "
+              f"| ~{to:.0f} s extrapolated, 1 thread; max err {err:.1f} x 2^-53 S |", flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "dgemm":
+        dgemm_rows()
+        sys.exit(0)
     main()
