@@ -67,6 +67,10 @@ struct GemmArgs {
     int32_t num_kb;     // K-blocks of BK
     int32_t kc;         // K-blocks per TMEM chunk (promotion interval); >= num_kb: no promotion
     int32_t tiles_m, tiles_n, group_m;
+    // Work items: items [0, full_items) are whole tiles in raster order; the
+    // remaining tiles (the last, partial wave) are split into two half-width
+    // (BN/2 column) items each, so the tail wave takes half a tile time.
+    int32_t full_items, num_items;
     int32_t use_clc;    // 1: one cluster per tile + cluster launch control; 0: static persistent stride
     int32_t *wave_sync; // static stride only, optional: arrival counters (zeroed per launch), one per
                         // (wave, K phase of sync_kb K-blocks)
@@ -140,6 +144,18 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
     const int r = t - g * per_group;
     tm = first + r % gsz;
     tn = r / gsz;
+}
+
+// Work item w -> tile (tm, tn) and part: -1 = whole tile, 0/1 = column half.
+__device__ __forceinline__ void decode_item(int w, const GemmArgs &a, int &tm, int &tn, int &part) {
+    if (w < a.full_items) {
+        tile_coords(w, a.tiles_m, a.tiles_n, a.group_m, tm, tn);
+        part = -1;
+    } else {
+        const int h = w - a.full_items;
+        tile_coords(a.full_items + (h >> 1), a.tiles_m, a.tiles_n, a.group_m, tm, tn);
+        part = h & 1;
+    }
 }
 
 // Write one 32 x 32 piece of C held as (thread = row, v[i] = column i) through
@@ -238,7 +254,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
-    const int num_tiles = args.tiles_m * args.tiles_n;
+    const int num_items = args.num_items;
     const int num_kb = args.num_kb;
     const int kc = args.kc;
 
@@ -253,12 +269,15 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t ph = 0;
         SchedReader<CG> sched;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
-            int tm, tn;
-            tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
+            int tm, tn, part;
+            decode_item(t, args, tm, tn, part);
             const int32_t m0 = tm * Cfg::TILE_M + rank * ROWS_PER_CTA;
-            const int32_t n0 = tn * BN + rank * Cfg::B_ROWS;
+            // half items need B_ROWS/2 rows per CTA; the full box is loaded (the
+            // extra rows are never read by the N = BN/2 MMA)
+            const int32_t n0 = part < 0 ? tn * BN + rank * Cfg::B_ROWS
+                                        : tn * BN + part * (BN / 2) + rank * (Cfg::B_ROWS / 2);
             const int wave = t / num_clusters;
-            const int wave_target = CG * min(num_clusters, num_tiles - wave * num_clusters);
+            const int wave_target = CG * min(num_clusters, num_items - wave * num_clusters);
             const int phases = (num_kb + args.sync_kb - 1) / args.sync_kb;
             for (int kb = 0; kb < num_kb; kb++) {
                 if (args.wave_sync != nullptr && kb % args.sync_kb == 0) {
@@ -303,7 +322,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t ph = 0, cph = 0;
         int t = cluster_id;
         for (;;) {
-            if (t >= num_tiles) t = -1;
+            if (t >= num_items) t = -1;
             ptx::mbar_wait_cluster(&sempty[slot], ph ^ 1);
             if (lane == 0) {
 #pragma unroll
@@ -331,11 +350,13 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1 && rank == 0) {
         // ======================= MMA issuer (leader CTA) =======================
-        constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::TILE_M, BN);
+        constexpr uint32_t idesc_full = ptx::idesc_tf32(Cfg::TILE_M, BN);
+        constexpr uint32_t idesc_half = ptx::idesc_tf32(Cfg::TILE_M, BN / 2);
         int s = 0;
         uint32_t ph = 0, buf = 0, aph = 0;
         SchedReader<CG> sched;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
+            const uint32_t idesc = t < args.full_items ? idesc_full : idesc_half;
             for (int kb = 0; kb < num_kb; kb++) {
                 const int kin = kb % kc;
                 const bool chunk_first = kin == 0;
@@ -388,25 +409,29 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t q = warp & 3;        // TMEM lane quarter this warp may access
         const uint32_t half = e >> 2;       // column half of the accumulator
         float *tbuf = epi + e * (32 * 32);
-        const uint32_t tq = tmem_base + ((32u * q) << 16) + half * Cfg::COLS_PER_WARP;
+        const uint32_t tq0 = tmem_base + ((32u * q) << 16);
         uint32_t buf = 0, aph = 0;
         const int nchunks = (num_kb + kc - 1) / kc;
         SchedReader<CG> sched;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
-            int tm, tn;
-            tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
+            int tm, tn, part;
+            decode_item(t, args, tm, tn, part);
+            // whole tile: this warp owns columns [half*BN/2, +BN/2); half item: [half*BN/4, +BN/4)
+            const int cpw = part < 0 ? Cfg::COLS_PER_WARP : Cfg::COLS_PER_WARP / 2;
+            const int pieces = cpw / 32;
+            const uint32_t tq = tq0 + half * cpw;
             const int64_t row0 = (int64_t)tm * Cfg::TILE_M + rank * ROWS_PER_CTA + 32 * q;
-            const int64_t col0 = (int64_t)tn * BN + half * Cfg::COLS_PER_WARP;
+            const int64_t col0 = (int64_t)tn * BN + (part < 0 ? 0 : part * (BN / 2)) + half * cpw;
             if (nchunks == 1) {
                 // whole K accumulated in TMEM: stream 32-column pieces to C
                 ptx::mbar_wait(&tfull[buf], aph);
                 ptx::tc_fence_after();
 #pragma unroll 1
-                for (int qq = 0; qq < Cfg::PIECES; qq++) {
+                for (int qq = 0; qq < pieces; qq++) {
                     uint32_t v[32];
                     ptx::tmem_ld_32x32b_x32(tq + buf * BN + qq * 32, v);
                     ptx::tmem_ld_wait();
-                    if (qq == Cfg::PIECES - 1) {  // accumulator buffer free for the next tile
+                    if (qq == pieces - 1) {  // accumulator buffer free for the next tile
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
@@ -425,15 +450,17 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t taddr = tq + buf * BN;
 #pragma unroll
                     for (int qq = 0; qq < Cfg::PIECES; qq++) {
-                        uint32_t v[32];
-                        ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v);
-                        ptx::tmem_ld_wait();
-                        if (c == 0) {
+                        if (qq < pieces) {
+                            uint32_t v[32];
+                            ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v);
+                            ptx::tmem_ld_wait();
+                            if (c == 0) {
 #pragma unroll
-                            for (int i = 0; i < 32; i++) acc[qq][i] = __uint_as_float(v[i]);
-                        } else {
+                                for (int i = 0; i < 32; i++) acc[qq][i] = __uint_as_float(v[i]);
+                            } else {
 #pragma unroll
-                            for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v[i]);
+                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v[i]);
+                            }
                         }
                     }
                     ptx::tc_fence_before();
@@ -444,10 +471,12 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 }
 #pragma unroll
                 for (int qq = 0; qq < Cfg::PIECES; qq++) {
-                    uint32_t v[32];
+                    if (qq < pieces) {
+                        uint32_t v[32];
 #pragma unroll
-                    for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
-                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v);
+                        for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
+                        store_piece(args, tbuf, lane, row0, col0 + qq * 32, v);
+                    }
                 }
             }
         }

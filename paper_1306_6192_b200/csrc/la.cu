@@ -136,7 +136,10 @@ Operands operands_carve(void *ws, int64_t n, int64_t m, int64_t p, int passes) {
     return o;
 }
 
+static bool lo_raw() { return getenv("LA_LO_RAW") && atoi(getenv("LA_LO_RAW")) != 0; }  // A/B knob
+
 la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cudaStream_t st, int *launches) {
+    const bool raw = lo_raw();
     cudaEvent_t t0;
     la_status ts = timing_begin(st, &t0);
     if (ts != LA_OK) return ts;
@@ -146,17 +149,17 @@ la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cud
         if (ops.passes == 3)
             split_rows_vec4_kernel<3><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
                                                               reinterpret_cast<float4 *>(ops.a_hi),
-                                                              reinterpret_cast<float4 *>(ops.a_lo), count4);
+                                                              reinterpret_cast<float4 *>(ops.a_lo), count4, raw);
         else
             split_rows_vec4_kernel<1><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
                                                               reinterpret_cast<float4 *>(ops.a_hi),
-                                                              reinterpret_cast<float4 *>(ops.a_lo), count4);
+                                                              reinterpret_cast<float4 *>(ops.a_lo), count4, raw);
     } else {
         dim3 grid((unsigned)std::min<int64_t>((ops.mp + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
         if (ops.passes == 3)
-            split_rows_kernel<3><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            split_rows_kernel<3><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp, raw);
         else
-            split_rows_kernel<1><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            split_rows_kernel<1><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp, raw);
     }
     (*launches)++;
     cudaError_t e = cudaGetLastError();
@@ -174,9 +177,9 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     if (ts != LA_OK) return ts;
     float *hi = ops.b_hi + j0 * ops.mp, *lo = ops.b_lo + j0 * ops.mp;
     if (ops.passes == 3)
-        split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
+        split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
     else
-        split_transpose_kernel<1><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
+        split_transpose_kernel<1><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "split_b launch", __FILE__, __LINE__);
@@ -259,6 +262,21 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
         clusters = (int)tiles;
     }
+    // Tail split: if the last wave is at most half full, its tiles run as two
+    // half-width items each, so it takes half a tile time (n = 4096: 3.46 waves
+    // of 256x256 tiles -> 3.5 instead of 4).  Per-element accumulation order is
+    // unchanged (same K blocks, same promotion chunks), so results are bitwise
+    // identical with or without it.  LA_TAIL_SPLIT=0 disables.
+    args.full_items = args.num_items = (int32_t)tiles;
+    {
+        const char *te = getenv("LA_TAIL_SPLIT");
+        const bool tail_split = !args.use_clc && (te == nullptr || atoi(te) != 0);
+        const int64_t W = clusters, R = tiles % W;
+        if (tail_split && R > 0 && 2 * R <= W && tiles > W) {
+            args.full_items = (int32_t)(tiles - R);
+            args.num_items = (int32_t)(tiles + R);
+        }
+    }
     args.debug = getenv("LA_DEBUG_KERNEL") ? atoi(getenv("LA_DEBUG_KERNEL")) : 0;  // diagnostics only
     args.wave_sync = nullptr;
     args.sync_kb = args.num_kb;
@@ -275,7 +293,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     if (!args.use_clc && wave_sync > 0) {
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
         const int64_t phases = (args.num_kb + args.sync_kb - 1) / args.sync_kb;
-        const size_t nw = (size_t)((tiles + clusters - 1) / clusters * phases);
+        const size_t nw = (size_t)((args.num_items + clusters - 1) / clusters * phases);
         cudaError_t e = cudaMallocFromPoolAsync(&sync_buf, nw * sizeof(int32_t), g_state.pool, st);
         if (e != cudaSuccess) return cuda_fail(e, "wave sync buffer", __FILE__, __LINE__);
         e = cudaMemsetAsync(sync_buf, 0, nw * sizeof(int32_t), st);

@@ -21,11 +21,21 @@
 
 namespace la {
 
+// lo is stored rounded to TF32 as well (cvt.rna): the tensor pipe reads only the
+// TF32 bits of its fp32 operands, so this changes lo by at most half a TF32 ulp
+// (the per-product bound improves from 2^-21.06 to 2^-21.03 for 24-bit inputs,
+// SURVEY App. A) and stops 13 dead low bits from toggling through shared memory
+// and the operand path (LA_LO_RAW=1 restores the raw residual, for A/B runs).
+__device__ __forceinline__ float lo_part(float x, float h, bool raw) {
+    const float l = x - h;
+    return raw ? l : ptx::to_tf32_rna(l);
+}
+
 template <int PASSES>
-__device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64_t off) {
+__device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64_t off, bool raw = false) {
     const float h = ptx::to_tf32_rna(x);
     hi[off] = h;
-    if constexpr (PASSES == 3) lo[off] = x - h;
+    if constexpr (PASSES == 3) lo[off] = lo_part(x, h, raw);
 }
 
 // Row-major A, m % 4 == 0: flat float4 grid-stride loop (mp == m).
@@ -33,7 +43,7 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__restrict__ a,
                                                               float4 *__restrict__ hi,
                                                               float4 *__restrict__ lo,
-                                                              int64_t count4) {
+                                                              int64_t count4, bool lo_raw) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
          i += (int64_t)gridDim.x * blockDim.x) {
         const float4 x = __ldcs(a + i);
@@ -44,10 +54,10 @@ __global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__re
         h.w = ptx::to_tf32_rna(x.w);
         __stcg(hi + i, h);
         if constexpr (PASSES == 3) {
-            l.x = x.x - h.x;
-            l.y = x.y - h.y;
-            l.z = x.z - h.z;
-            l.w = x.w - h.w;
+            l.x = lo_part(x.x, h.x, lo_raw);
+            l.y = lo_part(x.y, h.y, lo_raw);
+            l.z = lo_part(x.z, h.z, lo_raw);
+            l.w = lo_part(x.w, h.w, lo_raw);
             __stcg(lo + i, l);
         }
     }
@@ -58,12 +68,12 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_rows_kernel(const float *__restrict__ a,
                                                          float *__restrict__ hi,
                                                          float *__restrict__ lo, int64_t n,
-                                                         int64_t m, int64_t mp) {
+                                                         int64_t m, int64_t mp, bool lo_raw) {
     for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
         for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < mp;
              c += (int64_t)gridDim.x * blockDim.x) {
             const float x = c < m ? a[r * m + c] : 0.0f;
-            split_store<PASSES>(x, hi, lo, r * mp + c);
+            split_store<PASSES>(x, hi, lo, r * mp + c, lo_raw);
         }
     }
 }
@@ -75,7 +85,8 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__restrict__ b,
                                                               float *__restrict__ hi,
                                                               float *__restrict__ lo, int64_t m,
-                                                              int64_t p, int64_t ldb, int64_t mp) {
+                                                              int64_t p, int64_t ldb, int64_t mp,
+                                                              bool lo_raw) {
     __shared__ float tile[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t j0 = (int64_t)blockIdx.x * 32;  // column of B = row of Bt
@@ -89,7 +100,7 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
 #pragma unroll
     for (int i = 0; i < 4; i++) {
         const int64_t j = j0 + ty + 8 * i, k = k0 + tx;
-        if (j < p && k < mp) split_store<PASSES>(tile[tx][ty + 8 * i], hi, lo, j * mp + k);
+        if (j < p && k < mp) split_store<PASSES>(tile[tx][ty + 8 * i], hi, lo, j * mp + k, lo_raw);
     }
 }
 
