@@ -311,15 +311,18 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
 }
 
 // Kernel choice: the CTA-pair 256 x 256 kernel (half the operand traffic per
-// FLOP) once it fills at least one wave of SM pairs, else the single-CTA
-// 128 x 128 kernel, which spreads small or thin problems over 4x more tiles.
+// FLOP) once there are at least 40 pair tiles, else the single-CTA 128 x 128
+// kernel, which spreads small or thin problems over 4x more tiles.  Measured
+// crossover (scripts/cg_choice.py): pair kernel faster from 49 pair tiles up
+// (n = 1792: 98 vs 130 us; n = 2048: 113 vs 151 us), single-CTA faster at <= 36
+// (n = 1536: 77 vs 85 us).
 static int choose_cta_group(int64_t n, int64_t pc) {
     if (const char *e = getenv("LA_CTA_GROUP")) {
         const int v = atoi(e);
         if (v == 1 || v == 2) return v;
     }
     const int64_t pair_tiles = ((n + 255) / 256) * ((pc + 255) / 256);
-    return pair_tiles >= g_state.sms / 2 ? 2 : 1;
+    return pair_tiles >= 40 ? 2 : 1;
 }
 
 la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
