@@ -289,7 +289,10 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // (profiles/energy_r01.md).  On by default for multi-wave problems with a
     // long K; LA_WAVE_SYNC=0 disables, =N sets the interval in K-blocks.
     const char *ws_env = getenv("LA_WAVE_SYNC");
-    int wave_sync = ws_env ? atoi(ws_env) : (tiles >= clusters && args.num_kb >= 64 ? 16 : 0);
+    // Never with an SM cap: the capped launch runs beside other kernels (NCCL in
+    // la_gemm_multi) and every participant of a wave must be resident.
+    int wave_sync = ws_env ? atoi(ws_env) : (args.num_kb >= 64 ? 16 : 0);
+    if (max_sms > 0) wave_sync = 0;
     if (!args.use_clc && wave_sync > 0) {
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
         const int64_t phases = (args.num_kb + args.sync_kb - 1) / args.sync_kb;

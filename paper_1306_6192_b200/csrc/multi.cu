@@ -95,6 +95,10 @@ la_status la_comm_init(const void *uid128, int rank, int ngpu) {
     memcpy(&id, uid128, sizeof id);
     ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
     cfg.blocking = 1;
+    // NCCL's kernels must fit in the SMs the GEMM leaves free while panels are
+    // in flight (la_gemm_multi launches the GEMM on sms - reserved SMs).
+    cfg.maxCTAs = reserved_sms() > 0 ? reserved_sms() : 8;
+    cfg.minCTAs = 1;
     LA_NCCL(ncclCommInitRankConfig(&g_comm.comm, ngpu, id, rank, &cfg));
     g_comm.rank = rank;
     g_comm.size = ngpu;
