@@ -176,7 +176,15 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     la_status ts = timing_begin(st, &t0);
     if (ts != LA_OK) return ts;
     float *hi = ops.b_hi + j0 * ops.mp, *lo = ops.b_lo + j0 * ops.mp;
-    if (ops.passes == 3)
+    const bool vec = pc % 4 == 0 && ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+    const bool T64 = vec && !(getenv("LA_SPLIT_T32") && atoi(getenv("LA_SPLIT_T32")) != 0);  // A/B knob
+    if (T64) {
+        dim3 g64((unsigned)((pc + 63) / 64), (unsigned)((ops.mp + 63) / 64));
+        if (ops.passes == 3)
+            split_transpose64_kernel<3><<<g64, 256, 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
+        else
+            split_transpose64_kernel<1><<<g64, 256, 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
+    } else if (ops.passes == 3)
         split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
     else
         split_transpose_kernel<1><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());

@@ -104,6 +104,55 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
     }
 }
 
+// B (m x p block, row stride ldb, p % 4 == 0, ldb % 4 == 0, 16-B aligned) ->
+// Bt (p x mp): 64 x 64 tiles, 16-byte loads along j and 16-byte stores along k
+// (each half-warp writes 256 contiguous bytes of one Bt row).  Block 256.
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_transpose64_kernel(const float *__restrict__ b,
+                                                                float *__restrict__ hi,
+                                                                float *__restrict__ lo, int64_t m,
+                                                                int64_t p, int64_t ldb, int64_t mp,
+                                                                bool lo_raw) {
+    __shared__ float tile[64][65];
+    const int tid = threadIdx.x;
+    const int64_t j0 = (int64_t)blockIdx.x * 64;  // columns of B = rows of Bt
+    const int64_t k0 = (int64_t)blockIdx.y * 64;  // rows of B = columns of Bt
+    // load: 64 rows (k) x 16 float4 (j); thread -> (row r = tid / 16 + 16 i, col4 c = tid % 16)
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int r = tid / 16 + 16 * i, c = (tid % 16) * 4;
+        const int64_t k = k0 + r, j = j0 + c;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < m && j < p) v = __ldcs(reinterpret_cast<const float4 *>(b + k * ldb + j));  // p % 4 == 0
+        tile[r][c] = v.x;
+        tile[r][c + 1] = v.y;
+        tile[r][c + 2] = v.z;
+        tile[r][c + 3] = v.w;
+    }
+    __syncthreads();
+    // store: 64 rows (j) x 16 float4 (k); thread -> (row j = tid / 16 + 16 i, k4 = tid % 16)
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int jr = tid / 16 + 16 * i, kc = (tid % 16) * 4;
+        const int64_t j = j0 + jr, k = k0 + kc;
+        if (j >= p || k >= mp) continue;  // mp % 4 == 0, so a float4 never straddles mp
+        float x[4] = {tile[kc][jr], tile[kc + 1][jr], tile[kc + 2][jr], tile[kc + 3][jr]};
+        float4 h, l;
+        h.x = ptx::to_tf32_rna(x[0]);
+        h.y = ptx::to_tf32_rna(x[1]);
+        h.z = ptx::to_tf32_rna(x[2]);
+        h.w = ptx::to_tf32_rna(x[3]);
+        __stcg(reinterpret_cast<float4 *>(hi + j * mp + k), h);
+        if constexpr (PASSES == 3) {
+            l.x = lo_part(x[0], h.x, lo_raw);
+            l.y = lo_part(x[1], h.y, lo_raw);
+            l.z = lo_part(x[2], h.z, lo_raw);
+            l.w = lo_part(x[3], h.w, lo_raw);
+            __stcg(reinterpret_cast<float4 *>(lo + j * mp + k), l);
+        }
+    }
+}
+
 }  // namespace la
 
 namespace la {
