@@ -28,13 +28,17 @@ def nvcc_flags():
         "-Xptxas", "-v" if os.environ.get("LA_PTXAS_VERBOSE") else "-O3",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
         "-DLA_BUILD",
-    ]
+    ] + (["-DLA_DIAGNOSTICS"] if os.environ.get("LA_BUILD_DIAGNOSTICS") else [])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = SOURCES + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         [os.path.join(ROOT, "include", "la.h"), __file__]
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
+    stamp = LIB + ".flags"
+    flags_now = " ".join(nvcc_flags())
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags_now
+    if not force and same_flags and os.path.exists(LIB) and \
+            all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
     _, nccl_lib = _nccl_dirs()
     tmp = LIB + f".tmp{os.getpid()}"
@@ -44,6 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(flags_now)
     return LIB
 
 

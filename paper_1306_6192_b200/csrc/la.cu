@@ -285,7 +285,13 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
             args.num_items = (int32_t)(tiles + R);
         }
     }
-    args.debug = getenv("LA_DEBUG_KERNEL") ? atoi(getenv("LA_DEBUG_KERNEL")) : 0;  // diagnostics only
+#ifdef LA_DIAGNOSTICS
+    // Energy diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip
+    // MMAs.  Compiled in only with LA_BUILD_DIAGNOSTICS=1 at build time.
+    args.debug = getenv("LA_DEBUG_KERNEL") ? atoi(getenv("LA_DEBUG_KERNEL")) : 0;
+#else
+    args.debug = 0;
+#endif
     args.wave_sync = nullptr;
     args.sync_kb = args.num_kb;
     void *sync_buf = nullptr;
