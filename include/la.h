@@ -178,6 +178,17 @@ LA_API la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A
                         const float *d_B, float *d_C_local, float *d_C_full, int root,
                         int ngpu, void *stream);
 
+/* Collective over the communicator (every rank, same `bytes`): allocate a
+ * symmetric device buffer (ncclMemAlloc) registered as an NCCL window
+ * (NCCL_WIN_COLL_SYMMETRIC) and return it in *d_out.  Passing it as
+ * la_gemm_multi's d_C_full selects the FUSED all-gather: the GEMM epilogue
+ * stores this rank's rows straight into every rank's buffer over NVLink
+ * (load/store-accessible peers, up to 8) while later tiles compute, followed by
+ * one tiny cross-rank barrier instead of an ncclAllGather (NEXT item #1 of
+ * SURVEY 8(f)).  Freed by the next call, la_comm_init or la_finalize.
+ * Errors: NOT_INITIALIZED, INVALID_VALUE, NCCL. */
+LA_API la_status la_gather_alloc(int64_t bytes, void **d_out);
+
 /* Rows owned by `rank` of g: [*row0, *row0 + *rows).  Pure host arithmetic. */
 LA_API la_status la_shard_rows(int64_t n, int rank, int ngpu, int64_t *row0, int64_t *rows);
 

@@ -29,7 +29,7 @@ OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3}
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
            "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times", "la_cgemm",
-           "la_add", "la_dgemm")
+           "la_add", "la_dgemm", "la_gather_alloc")
 
 
 class LaError(RuntimeError):
@@ -52,6 +52,7 @@ def _load() -> ctypes.CDLL:
         "la_gemm_host": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_cgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_dgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_gather_alloc": ([i64, ctypes.POINTER(ctypes.c_void_p)], st),
         "la_add": ([i64, i64, vp, vp, vp, ctypes.c_int, vp], st),
         "la_get_unique_id": ([vp], st),
         "la_comm_init": ([vp, ctypes.c_int, ctypes.c_int], st),
@@ -281,6 +282,25 @@ def comm_init_from_process_group(group=None) -> None:
     import torch.distributed as dist
     uid = bootstrap_unique_id(group)
     comm_init(uid, dist.get_rank(group), dist.get_world_size(group))
+
+
+class _DeviceArray:
+    """Minimal __cuda_array_interface__ holder so torch can view library memory."""
+
+    def __init__(self, ptr, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def gather_buffer(n: int, p: int):
+    """la_gather_alloc: a symmetric n x p float32 C_full (collective); returns a
+    torch CUDA tensor viewing the library-owned buffer (valid until the next
+    gather_buffer / comm_init / finalize).  Passing it to gemm_multi as C_full
+    selects the fused all-gather epilogue."""
+    import torch
+    ptr = ctypes.c_void_p()
+    _check(_lib.la_gather_alloc(int(n) * int(p) * 4, ctypes.byref(ptr)), "la_gather_alloc")
+    return torch.as_tensor(_DeviceArray(ptr.value, (n, p)), device="cuda")
 
 
 def gemm_multi(n, m, p, A_local, B, C_local, C_full=None, root=0, ngpu=1, stream=None):

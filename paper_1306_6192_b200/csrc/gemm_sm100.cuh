@@ -34,6 +34,9 @@
 #pragma once
 #include <cstdint>
 
+#include <nccl.h>
+#include <nccl_device.h>
+
 #include "ptx.cuh"
 
 namespace la {
@@ -76,7 +79,16 @@ struct GemmArgs {
                         // (wave, K phase of sync_kb K-blocks)
     int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
     int32_t debug;      // diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip MMAs
+    // Fused all-gather (la_gemm_multi into a registered symmetric C_full): every
+    // output element (r, c) is also stored at row gather_row0 + r, column
+    // gather_col0 + c (row stride gather_ld) of each LSA peer's window, i.e.
+    // straight into every rank's C_full over NVLink, while the GEMM runs.
+    const void *gather_win;  // ncclWindow_t (device-resident struct) or nullptr
+    int32_t gather_peers;    // LSA team size (<= MAX_GATHER_PEERS)
+    int64_t gather_row0, gather_col0, gather_ld;
 };
+
+constexpr int MAX_GATHER_PEERS = 8;  // one NVLink / NVSwitch domain of 8 GPUs
 
 // Optional K-phase alignment of the static persistent schedule: before the
 // first load of its w-th tile every producer arrives on counter w and waits
@@ -169,7 +181,8 @@ __device__ __forceinline__ float *row_ptr(const GemmArgs &args, int64_t r) {
 }
 
 __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, uint32_t lane, int64_t row0,
-                                            int64_t col0, const uint32_t (&v)[32]) {
+                                            int64_t col0, const uint32_t (&v)[32],
+                                            float *const *gbase = nullptr) {
 #pragma unroll
     for (int i = 0; i < 32; i++) tbuf[lane * 32 + (i ^ lane)] = __uint_as_float(v[i]);
     __syncwarp();
@@ -188,6 +201,14 @@ __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, u
         } else {
             for (int rr = 0; rr < rows; rr++)
                 row_ptr(args, row0 + rr)[col * args.cstride] = tbuf[rr * 32 + (lane ^ rr)];
+        }
+        if (gbase != nullptr) {
+            // the same 32 x 32 piece into every rank's C_full (128-B row segments over NVLink)
+            const int64_t goff = (args.gather_row0 + row0) * args.gather_ld + args.gather_col0 + col;
+            for (int pe = 0; pe < args.gather_peers; pe++) {
+                float *gp = gbase[pe] + goff;
+                for (int rr = 0; rr < rows; rr++) gp[rr * args.gather_ld] = tbuf[rr * 32 + (lane ^ rr)];
+            }
         }
     }
     __syncwarp();
@@ -217,6 +238,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(clc_bar + 1);
     int32_t *stile = reinterpret_cast<int32_t *>(tmem_holder + 4);         // [SCHED_SLOTS]
     uint8_t *clc_resp = reinterpret_cast<uint8_t *>(full) + 256;          // 16 B, 16-B aligned
+    float **gbase = reinterpret_cast<float **>(reinterpret_cast<uint8_t *>(full) + 320);  // [MAX_GATHER_PEERS]
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -246,6 +268,10 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&sempty[i], CG + 1 + CG * NUM_EPI_WARPS);  // producers, MMA, epilogue warps
         }
         ptx::mbar_init(clc_bar, 1);
+        if (args.gather_win != nullptr)
+            for (int pe = 0; pe < args.gather_peers; pe++)
+                gbase[pe] = static_cast<float *>(
+                    ncclGetLsaPointer(reinterpret_cast<ncclWindow_t>(const_cast<void *>(args.gather_win)), 0, pe));
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_holder, Cfg::TMEM_COLS);
@@ -410,6 +436,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t half = e >> 2;       // column half of the accumulator
         float *tbuf = epi + e * (32 * 32);
         const uint32_t tq0 = tmem_base + ((32u * q) << 16);
+        float *const *epi_gbase = args.gather_win != nullptr ? gbase : nullptr;
         uint32_t buf = 0, aph = 0;
         const int nchunks = (num_kb + kc - 1) / kc;
         SchedReader<CG> sched;
@@ -436,7 +463,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     }
-                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v);
+                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase);
                 }
                 buf ^= 1;
                 if (buf == 0) aph ^= 1;
@@ -475,11 +502,14 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         uint32_t v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
-                        store_piece(args, tbuf, lane, row0, col0 + qq * 32, v);
+                        store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase);
                     }
                 }
             }
         }
+        // fused gather: make this thread's peer stores visible system-wide before
+        // the kernel completes (the host orders a cross-rank barrier after it)
+        if (epi_gbase != nullptr) __threadfence_system();
     }
 
     ptx::tc_fence_before();

@@ -218,6 +218,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.cstride = out.cstride;
     args.half_rows = out.half_rows;
     args.half_off = out.half_off;
+    args.gather_win = out.gather_win;
+    args.gather_peers = out.gather_peers;
+    args.gather_row0 = out.gather_row0;
+    args.gather_col0 = out.gather_col0 + j0;
+    args.gather_ld = out.gather_ld;
     args.num_kb = (int32_t)((m + BK - 1) / BK);
     // Promotion only in 3xTF32: plain TF32's 2^-9 bound is 2^11 times looser than
     // the truncation bias of whole-K accumulation (~3 x 2^-20 S at K = 16384).

@@ -66,6 +66,10 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
 // Output addressing beyond plain row-major (see GemmArgs in gemm_sm100.cuh).
 struct OutSpec {
     int64_t cstride = 1, half_rows = 0, half_off = 0;
+    // fused all-gather into a registered symmetric window (see GemmArgs)
+    const void *gather_win = nullptr;
+    int gather_peers = 0;
+    int64_t gather_row0 = 0, gather_col0 = 0, gather_ld = 0;
 };
 
 // C[:, j0:j0+pc] (n x pc block of a row-major matrix with row stride ldc) =

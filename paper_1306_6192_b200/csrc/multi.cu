@@ -17,6 +17,7 @@
 #include <cstring>
 #include <vector>
 
+#include "gemm_sm100.cuh"
 #include "la.h"
 #include "la_internal.h"
 
@@ -30,6 +31,12 @@ struct Comm {
     std::vector<cudaEvent_t> panel_ready;
     void *bstage = nullptr;  // packed B panels (m x p floats), every rank
     size_t bstage_bytes = 0;
+    // fused all-gather target: symmetric memory registered as an NCCL window
+    void *gather = nullptr;
+    size_t gather_bytes = 0;
+    ncclWindow_t gather_win = nullptr;
+    int lsa_size = 0;
+    int *barrier_buf = nullptr;  // 1 int for the post-GEMM cross-rank barrier
 };
 static Comm g_comm;
 
@@ -48,8 +55,26 @@ static la_status nccl_fail(ncclResult_t r, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call, __FILE__, __LINE__); \
     } while (0)
 
+static la_status gather_release() {
+    la_status s = LA_OK;
+    if (g_comm.gather_win) {
+        ncclResult_t r = ncclCommWindowDeregister(g_comm.comm, g_comm.gather_win);
+        if (r != ncclSuccess) s = nccl_fail(r, "ncclCommWindowDeregister");
+    }
+    if (g_comm.gather) {
+        ncclResult_t r = ncclMemFree(g_comm.gather);
+        if (r != ncclSuccess && s == LA_OK) s = nccl_fail(r, "ncclMemFree");
+    }
+    g_comm.gather = nullptr;
+    g_comm.gather_win = nullptr;
+    g_comm.gather_bytes = 0;
+    return s;
+}
+
 la_status comm_destroy() {
     la_status s = LA_OK;
+    if (g_comm.comm) gather_release();
+    if (g_comm.barrier_buf) cudaFree(g_comm.barrier_buf);
     if (g_comm.comm) {
         ncclResult_t r = ncclCommDestroy(g_comm.comm);
         if (r != ncclSuccess) s = nccl_fail(r, "ncclCommDestroy");
@@ -104,6 +129,30 @@ la_status la_comm_init(const void *uid128, int rank, int ngpu) {
     g_comm.size = ngpu;
     LA_CK(cudaStreamCreateWithFlags(&g_comm.stream, cudaStreamNonBlocking));
     LA_CK(cudaEventCreateWithFlags(&g_comm.start, cudaEventDisableTiming));
+    return LA_OK;
+}
+
+la_status la_gather_alloc(int64_t bytes, void **d_out) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (!g_comm.comm) return fail(LA_ERR_NOT_INITIALIZED, "la_comm_init has not been called");
+    if (bytes <= 0 || !d_out) return fail(LA_ERR_INVALID_VALUE, "bad gather buffer request");
+    la_status s = gather_release();
+    if (s != LA_OK) return s;
+    const size_t sz = ((size_t)bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
+                      NCCL_WIN_REQUIRED_ALIGNMENT;
+    LA_NCCL(ncclMemAlloc(&g_comm.gather, sz));
+    ncclResult_t r = ncclCommWindowRegister(g_comm.comm, g_comm.gather, sz, &g_comm.gather_win,
+                                            NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+        ncclMemFree(g_comm.gather);
+        g_comm.gather = nullptr;
+        g_comm.gather_win = nullptr;
+        return nccl_fail(r, "ncclCommWindowRegister");
+    }
+    g_comm.gather_bytes = sz;
+    g_comm.lsa_size = ncclTeamLsa(g_comm.comm).nRanks;
+    if (!g_comm.barrier_buf) LA_CK(cudaMalloc(&g_comm.barrier_buf, sizeof(int)));
+    *d_out = g_comm.gather;
     return LA_OK;
 }
 
@@ -181,6 +230,26 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
         LA_CK(cudaEventRecord(g_comm.panel_ready[c], g_comm.stream));
     }
 
+    // Fused all-gather: C_full is the registered symmetric window and every
+    // rank is load/store reachable (one NVLink domain) -> the epilogue writes
+    // this rank's rows into every rank's C_full while the GEMM runs, instead of
+    // a separate ncclAllGather afterwards.
+    OutSpec out;
+    const bool fused = d_C_full != nullptr && d_C_full == g_comm.gather && g_comm.gather_win != nullptr &&
+                       g_comm.lsa_size == ngpu && ngpu <= MAX_GATHER_PEERS &&
+                       (size_t)(n * p) * sizeof(float) <= g_comm.gather_bytes;
+    if (fused) {
+        out.gather_win = g_comm.gather_win;
+        out.gather_peers = g_comm.lsa_size;
+        out.gather_row0 = row0;
+        out.gather_ld = p;
+        if (ngpu == 1)
+            if (const char *e = getenv("LA_TEST_GATHER_ROW0")) {  // test hook: exercise a non-zero row offset
+                out.gather_row0 = atoll(e);
+                if ((size_t)((out.gather_row0 + rows) * p) * sizeof(float) > g_comm.gather_bytes)
+                    return fail(LA_ERR_INVALID_VALUE, "LA_TEST_GATHER_ROW0 past the gather buffer");
+            }
+    }
     la_status s = split_a(rows, m, d_A_local, ops, st, &launches);
     const int reserve = ngpu > 1 ? reserved_sms() : 0;
     for (int64_t c = 0; c < P && s == LA_OK; c++) {
@@ -189,13 +258,18 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
         s = split_b(m, j0, w, bstage + m * j0, w, ops, st, &launches);
         if (s != LA_OK) break;
         const int max_sms = (c < P - 1 && reserve > 0) ? std::max(1, g_state.sms - reserve) : (int)g_state.max_sms;
-        s = gemm_run(rows, m, j0, w, ops, d_C_local, p, max_sms, st, &launches);
+        s = gemm_run(rows, m, j0, w, ops, d_C_local, p, max_sms, st, &launches, out);
     }
     e = cudaFreeAsync(ws, st);
     if (s != LA_OK) return s;
     if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);
-    if (d_C_full)
+    if (fused) {
+        // cross-rank barrier: every rank's GEMM (and its fenced peer stores) is
+        // complete before any rank's stream moves past this point
+        LA_NCCL(ncclAllReduce(g_comm.barrier_buf, g_comm.barrier_buf, 1, ncclInt, ncclSum, g_comm.comm, st));
+    } else if (d_C_full) {
         LA_NCCL(ncclAllGather(d_C_local, d_C_full, (size_t)(rows * p), ncclFloat, g_comm.comm, st));
+    }
     g_state.last_launches = launches;
     return LA_OK;
 }

@@ -111,3 +111,43 @@ def test_multi_errors(la1):
         la.gemm_multi(8, 8, 8, A, A, torch.empty(8, 8, device="cuda"), None, root=0, ngpu=2)
     with pytest.raises(la.LaError):
         la.gemm_multi(8, 8, 8, A, None, torch.empty(8, 8, device="cuda"), None, root=0, ngpu=1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("panels", [1, 3])
+def test_fused_gather_one_rank_bitwise(la1, panels):
+    """Fused GEMM -> all-gather (la_gather_alloc + la_gemm_multi): with one rank
+    the epilogue's peer stores land in this rank's own symmetric window, which
+    must equal la_gemm bitwise; C_local is written as well."""
+    la = la1
+    la.set_option("panels", panels)
+    n, m, p = 700, 500, 900
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    ref = la.gemm(A, B)
+    Cf = la.gather_buffer(n, p)
+    Cf.fill_(-1.0)
+    Cl = torch.empty(n, p, device="cuda")
+    la.gemm_multi(n, m, p, A, B, Cl, Cf, root=0, ngpu=1)
+    torch.cuda.synchronize()
+    assert torch.equal(Cl, ref)
+    assert torch.equal(Cf, ref)
+
+
+@pytest.mark.gpu
+def test_fused_gather_row_offset(la1, monkeypatch):
+    """Exercise a non-zero destination row (rank r writes rows r*n/g...) on one
+    GPU through the test hook LA_TEST_GATHER_ROW0: rows [7, 7+n) of a larger
+    symmetric buffer receive C, every other element keeps its sentinel."""
+    la = la1
+    la.set_option("panels", 2)
+    n, m, p = 300, 130, 520
+    A, B = inputs.pair(n, m, p, "integer", device="cuda")
+    ref = la.gemm(A, B)
+    Cf = la.gather_buffer(n + 20, p)
+    Cf.fill_(-7.0)
+    Cl = torch.empty(n, p, device="cuda")
+    monkeypatch.setenv("LA_TEST_GATHER_ROW0", "7")
+    la.gemm_multi(n, m, p, A, B, Cl, Cf, root=0, ngpu=1)
+    torch.cuda.synchronize()
+    assert torch.equal(Cf[7:7 + n], ref)
+    assert torch.all(Cf[:7] == -7.0) and torch.all(Cf[7 + n:] == -7.0)
