@@ -54,6 +54,8 @@ def _args():
     ap.add_argument("--mode", choices=["3xtf32", "tf32"], default="3xtf32")
     ap.add_argument("--inputs", choices=["random", "stress", "integer"], default="random")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--gather", choices=["none", "nccl", "fused"], default="none",
+                    help="N>1: also assemble C on every rank (ncclAllGather, or the fused epilogue)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
@@ -196,7 +198,8 @@ def _config(a, world):
             "n": a.n, "m": a.m, "p": a.p, "mode": a.mode,
             "inputs": f"{a.inputs} (counter-based generator, seed 13066192; inputs/)",
             "l2": "inputs larger than L2 (A, B, C 1 GiB each at n=16384); no flush needed",
-            "parallelism": f"rows{world}" if world > 1 else "single-gpu"}
+            "parallelism": f"rows{world}" if world > 1 else "single-gpu",
+            "gather": getattr(a, "gather", "none") if world > 1 else "n/a"}
 
 
 # ----------------------------------------------------------------- our arm
@@ -223,12 +226,15 @@ def run_ours(a, rank, world, local_rank):
     A = inputs.generate(n, m, inputs.ID_A, a.inputs, device="cuda", row_idx=list(range(row0, row0 + rows)))
     B = inputs.generate(m, p, inputs.ID_B, a.inputs, device="cuda") if (world == 1 or rank == 0) else None
     C = torch.empty(rows, p, device="cuda", dtype=torch.float32)
+    C_full = None
+    if a.gather != "none" and world > 1:
+        C_full = la.gather_buffer(n, p) if a.gather == "fused" else torch.empty(n, p, device="cuda")
 
     def step():
         if world == 1:
             la.gemm(A, B, out=C, stream=stream)
         else:
-            la.gemm_multi(n, m, p, A, B, C, None, root=0, ngpu=world, stream=stream)
+            la.gemm_multi(n, m, p, A, B, C, C_full, root=0, ngpu=world, stream=stream)
 
     la.set_option("kernel_timing", 1)
     for _ in range(a.warmup):
