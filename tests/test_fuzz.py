@@ -1,0 +1,58 @@
+"""Seeded shape fuzz on the GPU: random (n, m, p), log-uniform in [1, 1200],
+integer-valued inputs -> every product kind must equal its oracle exactly; and
+the two GEMM kernels (single CTA 128x128 vs CTA pair 256x256) must agree
+bitwise on the same inputs, because per-element accumulation order does not
+depend on the tile shape."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+RNG = np.random.default_rng(20261018)
+SHAPES = [tuple(int(x) for x in np.exp(RNG.uniform(0, np.log(1200), 3)).round().clip(1)) for _ in range(40)]
+
+
+@pytest.fixture(scope="module")
+def la():
+    import paper_1306_6192_b200 as la
+    la.init(0)
+    la.set_mode("3xtf32")
+    return la
+
+
+@pytest.mark.parametrize("n,m,p", SHAPES)
+def test_fuzz_gemm_integer_exact(la, n, m, p):
+    A = inputs.generate(n, m, 0, "integer", seed=n * 7919 + m * 31 + p)
+    B = inputs.generate(m, p, 1, "integer", seed=n * 7919 + m * 31 + p)
+    C = la.gemm(A.cuda(), B.cuda()).cpu().numpy()
+    assert np.array_equal(C, oracle.gemm(A.numpy(), B.numpy(), threads=8))
+
+
+@pytest.mark.parametrize("n,m,p", SHAPES[:12])
+def test_fuzz_kernels_agree_bitwise(la, n, m, p, monkeypatch):
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    out = {}
+    for cg in ("1", "2"):
+        monkeypatch.setenv("LA_CTA_GROUP", cg)
+        out[cg] = la.gemm(A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(out["1"], out["2"])
+
+
+@pytest.mark.parametrize("n,m,p", SHAPES[:10])
+def test_fuzz_cgemm_dgemm_integer_exact(la, n, m, p):
+    re = inputs.generate(n, 2 * m, 0, "integer")
+    A = torch.view_as_complex(re.view(n, m, 2)).contiguous()
+    re = inputs.generate(m, 2 * p, 1, "integer")
+    B = torch.view_as_complex(re.view(m, p, 2)).contiguous()
+    C = la.cgemm(A.cuda(), B.cuda()).cpu().numpy()
+    assert np.array_equal(C, oracle.cgemm(A.numpy(), B.numpy()))
+    Ad = inputs.generate_f64(n, m, 0, "integer")
+    Bd = inputs.generate_f64(m, p, 1, "integer")
+    D = la.dgemm(Ad.cuda(), Bd.cuda()).cpu().numpy()
+    assert np.array_equal(D, oracle.dgemm(Ad.numpy(), Bd.numpy()))
