@@ -74,6 +74,12 @@ struct GemmArgs {
     // remaining tiles (the last, partial wave) are split into two half-width
     // (BN/2 column) items each, so the tail wave takes half a tile time.
     int32_t full_items, num_items;
+    // Split-K (few output tiles, long K): item w is K range w % ksplit of tile
+    // w / ksplit, K-blocks [s * kb_per, min(num_kb, (s + 1) * kb_per)); its
+    // promoted partial tile goes to partial + s * n * ldc (same layout as C),
+    // and a reduction kernel sums the ksplit partials in order.  ksplit == 1: off.
+    int32_t ksplit, kb_per;
+    float *partial;
     int32_t use_clc;    // 1: one cluster per tile + cluster launch control; 0: static persistent stride
     int32_t *wave_sync; // static stride only, optional: arrival counters (zeroed per launch), one per
                         // (wave, K phase of sync_kb K-blocks)
@@ -89,6 +95,18 @@ struct GemmArgs {
 };
 
 constexpr int MAX_GATHER_PEERS = 8;  // one NVLink / NVSwitch domain of 8 GPUs
+
+// Split-K reduction: C = ((P_0 + P_1) + P_2) + ... elementwise, in split order
+// (deterministic).  HBM-bound, 4 (ksplit + 1) bytes per element.
+static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ part, float *__restrict__ C,
+                                                            int64_t count, int ksplit) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = part[i];
+        for (int s = 1; s < ksplit; s++) acc += part[(int64_t)s * count + i];
+        C[i] = acc;
+    }
+}
 
 // Optional K-phase alignment of the static persistent schedule: before the
 // first load of its w-th tile every producer arrives on counter w and waits
@@ -158,8 +176,21 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
     tn = r / gsz;
 }
 
-// Work item w -> tile (tm, tn) and part: -1 = whole tile, 0/1 = column half.
-__device__ __forceinline__ void decode_item(int w, const GemmArgs &a, int &tm, int &tn, int &part) {
+// Work item w -> tile (tm, tn), part (-1 = whole tile, 0/1 = column half) and
+// its K-block range [kb0, kb1) and split index ks.
+__device__ __forceinline__ void decode_item(int w, const GemmArgs &a, int &tm, int &tn, int &part, int &kb0,
+                                            int &kb1, int &ks) {
+    if (a.ksplit > 1) {
+        ks = w % a.ksplit;
+        tile_coords(w / a.ksplit, a.tiles_m, a.tiles_n, a.group_m, tm, tn);
+        part = -1;
+        kb0 = ks * a.kb_per;
+        kb1 = min(a.num_kb, kb0 + a.kb_per);
+        return;
+    }
+    ks = 0;
+    kb0 = 0;
+    kb1 = a.num_kb;
     if (w < a.full_items) {
         tile_coords(w, a.tiles_m, a.tiles_n, a.group_m, tm, tn);
         part = -1;
@@ -182,7 +213,7 @@ __device__ __forceinline__ float *row_ptr(const GemmArgs &args, int64_t r) {
 
 __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, uint32_t lane, int64_t row0,
                                             int64_t col0, const uint32_t (&v)[32],
-                                            float *const *gbase = nullptr) {
+                                            float *const *gbase = nullptr, float *cbase = nullptr) {
 #pragma unroll
     for (int i = 0; i < 32; i++) tbuf[lane * 32 + (i ^ lane)] = __uint_as_float(v[i]);
     __syncwarp();
@@ -191,7 +222,7 @@ __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, u
     if (col < args.p && rem > 0) {
         const int rows = rem < 32 ? (int)rem : 32;
         if (args.half_rows == 0 && args.cstride == 1) {
-            float *cp = args.C + row0 * args.ldc + col;
+            float *cp = (cbase ? cbase : args.C) + row0 * args.ldc + col;
             if (rows == 32) {
 #pragma unroll 4
                 for (int rr = 0; rr < 32; rr++) cp[rr * args.ldc] = tbuf[rr * 32 + (lane ^ rr)];
@@ -295,8 +326,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t ph = 0;
         SchedReader<CG> sched;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
-            int tm, tn, part;
-            decode_item(t, args, tm, tn, part);
+            int tm, tn, part, kb0, kb1, ks;
+            decode_item(t, args, tm, tn, part, kb0, kb1, ks);
             const int32_t m0 = tm * Cfg::TILE_M + rank * ROWS_PER_CTA;
             // half items need B_ROWS/2 rows per CTA; the full box is loaded (the
             // extra rows are never read by the N = BN/2 MMA)
@@ -305,7 +336,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const int wave = t / num_clusters;
             const int wave_target = CG * min(num_clusters, num_items - wave * num_clusters);
             const int phases = (num_kb + args.sync_kb - 1) / args.sync_kb;
-            for (int kb = 0; kb < num_kb; kb++) {
+            for (int kb = kb0; kb < kb1; kb++) {
                 if (args.wave_sync != nullptr && kb % args.sync_kb == 0) {
                     if (lane == 0) wave_barrier(args.wave_sync + wave * phases + kb / args.sync_kb, wave_target);
                     __syncwarp();
@@ -383,10 +414,12 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         SchedReader<CG> sched;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
             const uint32_t idesc = t < args.full_items ? idesc_full : idesc_half;
-            for (int kb = 0; kb < num_kb; kb++) {
-                const int kin = kb % kc;
+            int tm_, tn_, part_, kb0, kb1, ks_;
+            decode_item(t, args, tm_, tn_, part_, kb0, kb1, ks_);
+            for (int kb = kb0; kb < kb1; kb++) {
+                const int kin = (kb - kb0) % kc;
                 const bool chunk_first = kin == 0;
-                const bool chunk_last = kin == kc - 1 || kb == num_kb - 1;
+                const bool chunk_last = kin == kc - 1 || kb == kb1 - 1;
                 if (chunk_first) {
                     if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[buf], aph ^ 1);
                     else ptx::mbar_wait(&tempty[buf], aph ^ 1);
@@ -438,11 +471,12 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t tq0 = tmem_base + ((32u * q) << 16);
         float *const *epi_gbase = args.gather_win != nullptr ? gbase : nullptr;
         uint32_t buf = 0, aph = 0;
-        const int nchunks = (num_kb + kc - 1) / kc;
         SchedReader<CG> sched;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
-            int tm, tn, part;
-            decode_item(t, args, tm, tn, part);
+            int tm, tn, part, kb0, kb1, ks;
+            decode_item(t, args, tm, tn, part, kb0, kb1, ks);
+            const int nchunks = (kb1 - kb0 + kc - 1) / kc;
+            float *cbase = args.ksplit > 1 ? args.partial + (int64_t)ks * args.n * args.ldc : nullptr;
             // whole tile: this warp owns columns [half*BN/2, +BN/2); half item: [half*BN/4, +BN/4)
             const int cpw = part < 0 ? Cfg::COLS_PER_WARP : Cfg::COLS_PER_WARP / 2;
             const int pieces = cpw / 32;
@@ -463,7 +497,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     }
-                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase);
+                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase, cbase);
                 }
                 buf ^= 1;
                 if (buf == 0) aph ^= 1;
@@ -502,7 +536,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         uint32_t v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
-                        store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase);
+                        store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase, cbase);
                     }
                 }
             }

@@ -275,15 +275,50 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
         clusters = (int)tiles;
     }
+    // Split-K: fewer tiles than half the clusters and a long K -> each tile's K
+    // range is cut into S pieces (at least 8 K-blocks each) computed by
+    // different clusters; partial tiles go to a workspace and are summed in
+    // order by splitk_reduce_kernel.  Plain real outputs from la_gemm only
+    // (OutSpec::splitk_ok).  LA_SPLIT_K=0 disables, =S forces S.
+    args.ksplit = 1;
+    args.kb_per = args.num_kb;
+    args.partial = nullptr;
+    void *part_buf = nullptr;
+    {
+        const char *se = getenv("LA_SPLIT_K");
+        const int forced = se ? atoi(se) : -1;
+        int S = 1;
+        if (out.splitk_ok && !args.use_clc && max_sms <= 0 && out.cstride == 1 && out.half_rows == 0 &&
+            out.gather_win == nullptr && ldc == pc && forced != 0) {
+            if (forced > 1) S = forced;
+            else if (2 * tiles <= max_clusters && args.num_kb >= 16)
+                S = (int)std::min<int64_t>(std::min<int64_t>(max_clusters / tiles, args.num_kb / 8), 16);
+        }
+        if (S > 1) {
+            args.kb_per = (args.num_kb + S - 1) / S;
+            S = (args.num_kb + args.kb_per - 1) / args.kb_per;
+        }
+        if (S > 1) {
+            args.ksplit = S;
+            const size_t pbytes = (size_t)S * (size_t)(n * pc) * sizeof(float);
+            cudaError_t e = cudaMallocFromPoolAsync(&part_buf, pbytes, g_state.pool, st);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(LA_ERR_OUT_OF_MEMORY, "split-K partials of %zu bytes", pbytes);
+            }
+            args.partial = static_cast<float *>(part_buf);
+            clusters = (int)std::min<int64_t>((int64_t)tiles * S, max_clusters);
+        }
+    }
     // Tail split: if the last wave is at most half full, its tiles run as two
     // half-width items each, so it takes half a tile time (n = 4096: 3.46 waves
     // of 256x256 tiles -> 3.5 instead of 4).  Per-element accumulation order is
     // unchanged (same K blocks, same promotion chunks), so results are bitwise
     // identical with or without it.  LA_TAIL_SPLIT=0 disables.
-    args.full_items = args.num_items = (int32_t)tiles;
+    args.full_items = args.num_items = (int32_t)(tiles * args.ksplit);
     {
         const char *te = getenv("LA_TAIL_SPLIT");
-        const bool tail_split = !args.use_clc && (te == nullptr || atoi(te) != 0);
+        const bool tail_split = !args.use_clc && args.ksplit == 1 && (te == nullptr || atoi(te) != 0);
         const int64_t W = clusters, R = tiles % W;
         if (tail_split && R > 0 && 2 * R <= W && tiles > W) {
             args.full_items = (int32_t)(tiles - R);
@@ -311,7 +346,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // Never with an SM cap: the capped launch runs beside other kernels (NCCL in
     // la_gemm_multi) and every participant of a wave must be resident.
     int wave_sync = ws_env ? atoi(ws_env) : (args.num_kb >= 64 ? 16 : 0);
-    if (max_sms > 0) wave_sync = 0;
+    if (max_sms > 0 || args.ksplit > 1) wave_sync = 0;
     if (!args.use_clc && wave_sync > 0) {
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
         const int64_t phases = (args.num_kb + args.sync_kb - 1) / args.sync_kb;
@@ -329,7 +364,21 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
     if (sync_buf) cudaFreeAsync(sync_buf, st);
-    return timing_end(st, t0, TIMED_GEMM);
+    la_status rs = timing_end(st, t0, TIMED_GEMM);
+    if (rs != LA_OK) return rs;
+    if (args.ksplit > 1) {
+        const int64_t count = n * pc;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)g_state.sms * 8));
+        cudaEvent_t t1;
+        if ((rs = timing_begin(st, &t1)) != LA_OK) return rs;
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(args.partial, args.C, count, args.ksplit);
+        (*launches)++;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "split-K reduce launch", __FILE__, __LINE__);
+        cudaFreeAsync(part_buf, st);
+        return timing_end(st, t1, TIMED_SPLIT);  // counted with the auxiliary passes
+    }
+    return LA_OK;
 }
 
 // Kernel choice: the CTA-pair 256 x 256 kernel (half the operand traffic per
@@ -390,7 +439,9 @@ static la_status gemm_impl(int64_t n, int64_t m, int64_t p, const float *A, cons
     const Operands ops = operands_carve(ws, n, m, p, passes);
     la_status s = split_a(n, m, A, ops, st, launches);
     if (s == LA_OK) s = split_b(m, 0, p, B, p, ops, st, launches);
-    if (s == LA_OK) s = gemm_run(n, m, 0, p, ops, C, ldc, (int)g_state.max_sms, st, launches);
+    OutSpec out;
+    out.splitk_ok = true;
+    if (s == LA_OK) s = gemm_run(n, m, 0, p, ops, C, ldc, (int)g_state.max_sms, st, launches, out);
     e = cudaFreeAsync(ws, st);
     if (s == LA_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);
     return s;

@@ -70,6 +70,10 @@ struct OutSpec {
     const void *gather_win = nullptr;
     int gather_peers = 0;
     int64_t gather_row0 = 0, gather_col0 = 0, gather_ld = 0;
+    // la_gemm may split K across clusters when there are few output tiles (the
+    // multi-GPU path never does, so its result stays bitwise equal to la_gemm
+    // without split-K)
+    bool splitk_ok = false;
 };
 
 // C[:, j0:j0+pc] (n x pc block of a row-major matrix with row stride ldc) =

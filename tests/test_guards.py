@@ -37,7 +37,7 @@ def _check_guards(buf, g, count):
 
 
 SHAPES = [(1, 1, 1), (17, 33, 5), (129, 257, 255), (257, 100, 383), (300, 70, 513), (1000, 64, 1500),
-          (2305, 96, 2100), (4352, 64, 4360)]
+          (2305, 96, 2100), (4352, 64, 4360), (130, 3000, 250), (40, 16384, 70)]   # last two: split-K
 
 
 @pytest.mark.parametrize("n,m,p", SHAPES)
@@ -96,7 +96,7 @@ def test_add_guards(la, rows, cols):
     assert torch.equal(C, A + B)
 
 
-def test_multi_panel_guards(la):
+def test_multi_panel_guards(la, monkeypatch):
     la.comm_init(la.get_unique_id(), 0, 1)
     la.set_option("panels", 3)
     try:
@@ -107,6 +107,7 @@ def test_multi_panel_guards(la):
         la.gemm_multi(n, m, p, A, B, C, None, root=0, ngpu=1)
         torch.cuda.synchronize()
         _check_guards(buf, g, n * p)
+        monkeypatch.setenv("LA_SPLIT_K", "0")
         assert torch.equal(C, la.gemm(A, B))
     finally:
         la.set_option("panels", 4)

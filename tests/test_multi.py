@@ -87,9 +87,10 @@ def la1():
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,m,p,panels", [(512, 384, 640, 1), (512, 384, 640, 3), (300, 1000, 1500, 4),
                                           (4096, 2048, 4096, 4)])
-def test_multi_one_rank_bitwise_equals_single(la1, n, m, p, panels):
+def test_multi_one_rank_bitwise_equals_single(la1, n, m, p, panels, monkeypatch):
     la = la1
     la.set_option("panels", panels)
+    monkeypatch.setenv("LA_SPLIT_K", "0")   # the multi path never splits K
     A, B = inputs.pair(n, m, p, "stress", device="cuda")
     ref = la.gemm(A, B)
     Cl = torch.empty(n, p, device="cuda")
@@ -115,12 +116,13 @@ def test_multi_errors(la1):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("panels", [1, 3])
-def test_fused_gather_one_rank_bitwise(la1, panels):
+def test_fused_gather_one_rank_bitwise(la1, panels, monkeypatch):
     """Fused GEMM -> all-gather (la_gather_alloc + la_gemm_multi): with one rank
     the epilogue's peer stores land in this rank's own symmetric window, which
     must equal la_gemm bitwise; C_local is written as well."""
     la = la1
     la.set_option("panels", panels)
+    monkeypatch.setenv("LA_SPLIT_K", "0")
     n, m, p = 700, 500, 900
     A, B = inputs.pair(n, m, p, "stress", device="cuda")
     ref = la.gemm(A, B)
@@ -140,6 +142,7 @@ def test_fused_gather_row_offset(la1, monkeypatch):
     symmetric buffer receive C, every other element keeps its sentinel."""
     la = la1
     la.set_option("panels", 2)
+    monkeypatch.setenv("LA_SPLIT_K", "0")
     n, m, p = 300, 130, 520
     A, B = inputs.pair(n, m, p, "integer", device="cuda")
     ref = la.gemm(A, B)

@@ -257,3 +257,23 @@ def test_n65536_indexing_sampled(la):
     del A, B, C
     torch.cuda.empty_cache()
     _check(As, Bs, got, "integer", "3xtf32")
+
+
+@pytest.mark.parametrize("n,m,p", [(512, 16384, 512), (1000, 2000, 1500), (64, 50000, 96), (300, 4096, 257)])
+def test_split_k_parity(la, n, m, p, monkeypatch):
+    """Few output tiles and a long K take the split-K path (partials reduced in
+    order): integer inputs exact, stress inputs within 2^-20, run-to-run bitwise,
+    and the forced split factors agree with the unsplit result within bound."""
+    A, B = inputs.pair(n, m, p, "integer", device="cuda")
+    rows = sorted({0, n // 3, n - 1})
+    C = la.gemm(A, B)
+    assert la.last_launch_count() == 4          # split A, split B, GEMM, reduction
+    _check(A[rows].cpu().numpy(), B.cpu().numpy(), C[rows].cpu().numpy(), "integer", "3xtf32")
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    C1, C2 = la.gemm(A, B), la.gemm(A, B)
+    assert torch.equal(C1, C2)
+    _check(A[rows].cpu().numpy(), B.cpu().numpy(), C1[rows].cpu().numpy(), "stress", "3xtf32")
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    C0 = la.gemm(A, B)
+    S = oracle.abs_scale(A[rows].cpu().numpy(), B.cpu().numpy())
+    assert np.all(np.abs(C0[rows].cpu().numpy().astype(np.float64) - C1[rows].cpu().numpy()) <= 2 * 2.0 ** -20 * S)
