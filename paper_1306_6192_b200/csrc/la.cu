@@ -194,6 +194,21 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     return timing_end(st, t0, TIMED_SPLIT);
 }
 
+// Split-K factor for a launch of `tiles` output tiles over `slots` concurrent
+// clusters: only with few tiles (at most half the slots) and a long K, at least
+// 8 K-blocks per piece, at most 16 pieces.
+static int splitk_factor(int64_t tiles, int64_t slots, int num_kb) {
+    if (const char *e = getenv("LA_SPLIT_K")) {
+        const int v = atoi(e);
+        if (v >= 0) return v <= 1 ? 1 : v;
+    }
+    if (2 * tiles > slots || num_kb < 16) return 1;
+    int S = (int)std::min<int64_t>(std::min<int64_t>(slots / tiles, num_kb / 8), 16);
+    if (S <= 1) return 1;
+    const int per = (num_kb + S - 1) / S;
+    return (num_kb + per - 1) / per;
+}
+
 template <int CG, int BN, int STAGES, int PASSES>
 static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C,
                              int64_t ldc, int max_sms, cudaStream_t st, int *launches, const OutSpec &out) {
@@ -285,21 +300,10 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.partial = nullptr;
     void *part_buf = nullptr;
     {
-        const char *se = getenv("LA_SPLIT_K");
-        const int forced = se ? atoi(se) : -1;
-        int S = 1;
-        if (out.splitk_ok && !args.use_clc && max_sms <= 0 && out.cstride == 1 && out.half_rows == 0 &&
-            out.gather_win == nullptr && ldc == pc && forced != 0) {
-            if (forced > 1) S = forced;
-            else if (2 * tiles <= max_clusters && args.num_kb >= 16)
-                S = (int)std::min<int64_t>(std::min<int64_t>(max_clusters / tiles, args.num_kb / 8), 16);
-        }
-        if (S > 1) {
-            args.kb_per = (args.num_kb + S - 1) / S;
-            S = (args.num_kb + args.kb_per - 1) / args.kb_per;
-        }
+        const int S = (out.splitk_ok && !args.use_clc) ? splitk_factor(tiles, max_clusters, args.num_kb) : 1;
         if (S > 1) {
             args.ksplit = S;
+            args.kb_per = (args.num_kb + S - 1) / S;
             const size_t pbytes = (size_t)S * (size_t)(n * pc) * sizeof(float);
             cudaError_t e = cudaMallocFromPoolAsync(&part_buf, pbytes, g_state.pool, st);
             if (e != cudaSuccess) {
@@ -381,24 +385,39 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     return LA_OK;
 }
 
-// Kernel choice: the CTA-pair 256 x 256 kernel (half the operand traffic per
-// FLOP) once there are at least 40 pair tiles, else the single-CTA 128 x 128
-// kernel, which spreads small or thin problems over 4x more tiles.  Measured
-// crossover (scripts/cg_choice.py): pair kernel faster from 49 pair tiles up
-// (n = 1792: 98 vs 130 us; n = 2048: 113 vs 151 us), single-CTA faster at <= 36
-// (n = 1536: 77 vs 85 us).
-static int choose_cta_group(int64_t n, int64_t pc) {
+// Kernel choice by a small cost model: time ~ waves x K-blocks per item x
+// cycles per K-block, with the single-CTA 128 x 128 kernel (768 tensor cycles
+// per K-block) charged 1.5x for its doubled operand traffic per flop (it is
+// L2-bound) against the CTA pair's 256 x 256 tiles (1536 cycles per K-block on
+// two SMs), each with its best split-K factor.  Measured checks
+// (scripts/cg_choice.py): pair wins from ~40 tiles up without split-K
+// (n = 2048: 108 vs 145 us), single-CTA for tiny problems (n = 256).
+static int choose_cta_group(int64_t n, int64_t pc, int num_kb, bool splitk_ok) {
     if (const char *e = getenv("LA_CTA_GROUP")) {
         const int v = atoi(e);
         if (v == 1 || v == 2) return v;
     }
-    const int64_t pair_tiles = ((n + 255) / 256) * ((pc + 255) / 256);
-    return pair_tiles >= 40 ? 2 : 1;
+    double cost[3] = {0, 0, 0};
+    for (int cg = 1; cg <= 2; cg++) {
+        const int64_t tm = 128 * cg, tn = cg == 2 ? 256 : 128;
+        const int64_t tiles = ((n + tm - 1) / tm) * ((pc + tn - 1) / tn);
+        const int64_t slots = g_state.sms / cg;
+        const int S = splitk_ok ? splitk_factor(tiles, slots, num_kb) : 1;
+        const int64_t items = tiles * S;
+        const int64_t kb_item = (num_kb + S - 1) / S;
+        const double waves = (double)((items + slots - 1) / slots);
+        cost[cg] = waves * kb_item * (cg == 2 ? 1536.0 : 768.0 * 1.5);
+    }
+    return cost[2] <= cost[1] ? 2 : 1;
 }
 
 la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
                    int max_sms, cudaStream_t st, int *launches, OutSpec out) {
-    const int cg = choose_cta_group(n, pc);
+    const int num_kb = (int)((m + BK - 1) / BK);
+    const bool splitk_ok = out.splitk_ok && max_sms <= 0 && out.cstride == 1 && out.half_rows == 0 &&
+                           out.gather_win == nullptr && ldc == pc;
+    out.splitk_ok = splitk_ok;
+    const int cg = choose_cta_group(n, pc, num_kb, splitk_ok);
     if (ops.passes == 3) {
         if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);

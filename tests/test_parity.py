@@ -267,7 +267,7 @@ def test_split_k_parity(la, n, m, p, monkeypatch):
     A, B = inputs.pair(n, m, p, "integer", device="cuda")
     rows = sorted({0, n // 3, n - 1})
     C = la.gemm(A, B)
-    assert la.last_launch_count() == 4          # split A, split B, GEMM, reduction
+    assert la.last_launch_count() == 4          # split A, split B, GEMM, split-K reduction
     _check(A[rows].cpu().numpy(), B.cpu().numpy(), C[rows].cpu().numpy(), "integer", "3xtf32")
     A, B = inputs.pair(n, m, p, "stress", device="cuda")
     C1, C2 = la.gemm(A, B), la.gemm(A, B)
