@@ -104,7 +104,9 @@ LA_API la_status la_get_option(la_option option, int64_t *value);
  *   d_A       : n x m row-major fp32, device;  d_B : m x p row-major fp32, device;
  *   d_C       : n x p row-major fp32, device, written exactly once per element.
  * Work: one split pass over A and over B into a library workspace, then one
- * persistent tcgen05 GEMM kernel.  Errors: NOT_INITIALIZED, INVALID_VALUE
+ * persistent tcgen05 GEMM kernel; problems with few output tiles and a long K
+ * split K across clusters and add one in-order reduction kernel (deterministic,
+ * integer inputs still exact).  Errors: NOT_INITIALIZED, INVALID_VALUE
  * (dims, NULL, C overlapping A or B), OUT_OF_MEMORY, CUDA. */
 LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B,
                   float *d_C, void *stream);
@@ -114,9 +116,10 @@ LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, cons
  * returns after everything completed.  The copies are pipelined with the
  * compute: B first, then A in row panels on a copy-in stream, each panel's
  * split + GEMM on `stream` as soon as it lands, each C panel copied back on a
- * copy-out stream while later panels compute.  Results are bitwise identical
- * to la_gemm.  Host buffers may be pageable or pinned (only pinned buffers
- * overlap).  Device staging is library-owned and reused.  Errors: as la_gemm. */
+ * copy-out stream while later panels compute.  Every element accumulates in
+ * la_gemm's order (bitwise identical to la_gemm whenever la_gemm does not split
+ * K).  Host buffers may be pageable or pinned (only pinned buffers overlap).
+ * Device staging is library-owned and reused.  Errors: as la_gemm. */
 LA_API la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B,
                        float *h_C, void *stream);
 
@@ -171,8 +174,8 @@ LA_API la_status la_comm_init(const void *uid128, int rank, int ngpu);
  *   d_C_full  : NULL, or n x p: if given, C is all-gathered (ncclAllGather)
  *               into it on every rank (requires n % g == 0).
  * All ranks pass identical n, m, p, root, ngpu.  Every output element is
- * accumulated in the same order as la_gemm, so results are bitwise identical
- * to the single-GPU path.  Errors: NOT_INITIALIZED, INVALID_VALUE (ngpu !=
+ * accumulated in the same order as la_gemm (which never splits K here), so
+ * results are bitwise identical to the single-GPU path without split-K.  Errors: NOT_INITIALIZED, INVALID_VALUE (ngpu !=
  * communicator size, dims), UNSUPPORTED (C_full with n % g != 0), NCCL, CUDA. */
 LA_API la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
                         const float *d_B, float *d_C_local, float *d_C_full, int root,

@@ -163,8 +163,10 @@ def test_host_entry_point(la):
 
 
 @pytest.mark.parametrize("n,m,p", [(2300, 700, 900), (4096, 1024, 2048)])
-def test_host_entry_point_pipelined_panels(la, n, m, p):
-    """n >= 2048 takes the pipelined row-panel path (ragged last panel at 2300)."""
+def test_host_entry_point_pipelined_panels(la, n, m, p, monkeypatch):
+    """n >= 2048 takes the pipelined row-panel path (ragged last panel at 2300);
+    bitwise equal to la_gemm without split-K (panels never split K)."""
+    monkeypatch.setenv("LA_SPLIT_K", "0")
     A, B = inputs.pair(n, m, p, "stress", device="cuda")
     ref = la.gemm(A, B).cpu()
     Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
