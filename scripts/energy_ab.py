@@ -40,7 +40,10 @@ for r in range(rounds):
         os.environ.update(base)
         for kv in v.split(","):
             k, val = kv.split("=", 1)
-            os.environ[k] = val
+            if k.startswith("opt:"):          # library option instead of an env knob
+                la.set_option(k[4:], int(val))
+            else:
+                os.environ[k] = val
         la.gemm(A, B, out=C)
         torch.cuda.synchronize()
         clks, stop = [], [False]
