@@ -279,3 +279,28 @@ def test_split_k_parity(la, n, m, p, monkeypatch):
     C0 = la.gemm(A, B)
     S = oracle.abs_scale(A[rows].cpu().numpy(), B.cpu().numpy())
     assert np.all(np.abs(C0[rows].cpu().numpy().astype(np.float64) - C1[rows].cpu().numpy()) <= 2 * 2.0 ** -20 * S)
+
+
+@pytest.mark.parametrize("a,b", [(-40, 13), (20, -30), (60, 50), (-50, -10)])
+def test_power_of_two_scaling_is_exact(la, a, b):
+    """Scaling by powers of two commutes exactly with every step of the path
+    (split hi/lo, exact 8-term tensor sums, truncation, promotion adds), so
+    C(2^a A, 2^b B) == 2^(a+b) C(A, B) bitwise while nothing under- or
+    overflows (products and their 2^-24 corrections stay normal)."""
+    A, B = inputs.pair(300, 1000, 260, "stress", device="cuda")
+    C = la.gemm(A, B)
+    Cs = la.gemm(A * 2.0 ** a, B * 2.0 ** b)
+    assert torch.equal(Cs, C * 2.0 ** (a + b))
+
+
+def test_dynamic_range_limit_documented(la):
+    """Below ~2^-100 per product the correction terms hi*lo' (2^-11 smaller, and
+    lo*hi' their own 2^-13 smaller parts) leave the fp32 normal range: the result
+    degrades toward plain TF32 accuracy (documented limit).
+    This pins the boundary: at 2^-45 per operand (products 2^-90) the 2^-20
+    bound still holds."""
+    A, B = inputs.pair(64, 2000, 64, "stress")
+    s = 2.0 ** -45
+    As, Bs = (A * s).numpy(), (B * s).numpy()
+    C = la.gemm(torch.from_numpy(As).cuda(), torch.from_numpy(Bs).cuda()).cpu().numpy()
+    _check(As, Bs, C, "stress", "3xtf32")
