@@ -483,7 +483,15 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint32_t tq = tq0 + half * cpw;
             const int64_t row0 = (int64_t)tm * Cfg::TILE_M + rank * ROWS_PER_CTA + 32 * q;
             const int64_t col0 = (int64_t)tn * BN + (part < 0 ? 0 : part * (BN / 2)) + half * cpw;
-            if (nchunks == 1) {
+            if (nchunks <= 0) {
+                // empty K range (never produced by the host's split-K plan): the
+                // partial contribution is zero; the MMA warp issues nothing for it
+                uint32_t v[32];
+#pragma unroll
+                for (int i = 0; i < 32; i++) v[i] = 0u;
+                for (int qq = 0; qq < pieces; qq++)
+                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase, cbase);
+            } else if (nchunks == 1) {
                 // whole K accumulated in TMEM: stream 32-column pieces to C
                 ptx::mbar_wait(&tfull[buf], aph);
                 ptx::tc_fence_after();

@@ -302,8 +302,14 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     {
         const int S = (out.splitk_ok && !args.use_clc) ? splitk_factor(tiles, max_clusters, args.num_kb) : 1;
         if (S > 1) {
-            args.ksplit = S;
+            // pieces of kb_per K-blocks; recount S from the piece size so every
+            // piece is non-empty ((S - 1) * kb_per < num_kb)
             args.kb_per = (args.num_kb + S - 1) / S;
+            const int S2 = (args.num_kb + args.kb_per - 1) / args.kb_per;
+            args.ksplit = S2;
+        }
+        if (args.ksplit > 1) {
+            const int S = args.ksplit;
             const size_t pbytes = (size_t)S * (size_t)(n * pc) * sizeof(float);
             cudaError_t e = cudaMallocFromPoolAsync(&part_buf, pbytes, g_state.pool, st);
             if (e != cudaSuccess) {

@@ -304,3 +304,15 @@ def test_dynamic_range_limit_documented(la):
     As, Bs = (A * s).numpy(), (B * s).numpy()
     C = la.gemm(torch.from_numpy(As).cuda(), torch.from_numpy(Bs).cuda()).cpu().numpy()
     _check(As, Bs, C, "stress", "3xtf32")
+
+
+@pytest.mark.parametrize("forced", ["2", "9", "16"])
+def test_split_k_forced_factors(la, forced, monkeypatch):
+    """Forced split factors, including ones that do not divide the K-block count
+    (129 K-blocks in 16 pieces): every piece non-empty, integer inputs exact."""
+    monkeypatch.setenv("LA_SPLIT_K", forced)
+    n, m, p = 200, 129 * 32, 300
+    A, B = inputs.pair(n, m, p, "integer", device="cuda")
+    C = la.gemm(A, B)
+    rows = [0, 101, 199]
+    _check(A[rows].cpu().numpy(), B.cpu().numpy(), C[rows].cpu().numpy(), "integer", "3xtf32")
