@@ -321,6 +321,10 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CTRL_REGS));
     if (warp == 0) {
         // ======================= TMA producer (both CTAs) =======================
+        // Programmatic dependent launch: everything above (barrier init, TMEM
+        // allocation, tensor-map prefetch, cluster sync) overlapped the split
+        // kernels' tail; the operands they write are read only after this.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const uint64_t pol = ptx::policy_evict_normal();
         int s = 0;
         uint32_t ph = 0;

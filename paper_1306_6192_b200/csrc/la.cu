@@ -369,9 +369,23 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     }
     cudaEvent_t t0;
     if ((s = timing_begin(st, &t0)) != LA_OK) return s;
-    kern<<<clusters * CG, NUM_THREADS, Cfg::SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, args);
+    // launched with programmatic stream serialization: the kernel's prologue may
+    // overlap the preceding split kernels; it waits (griddepcontrol.wait) before
+    // reading their output
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(clusters * CG));
+    lc.blockDim = dim3(NUM_THREADS);
+    lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    lc.stream = st;
+    cudaLaunchAttribute la_attr[1];
+    la_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la_attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = la_attr;
+    lc.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, ta_hi, ta_lo, tb_hi, tb_lo, args);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
     (*launches)++;
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
     if (sync_buf) cudaFreeAsync(sync_buf, st);
     la_status rs = timing_end(st, t0, TIMED_GEMM);

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__re
                                                               float4 *__restrict__ hi,
                                                               float4 *__restrict__ lo,
                                                               int64_t count4, bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
          i += (int64_t)gridDim.x * blockDim.x) {
         const float4 x = __ldcs(a + i);
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const float *__restrict
                                                          float *__restrict__ hi,
                                                          float *__restrict__ lo, int64_t n,
                                                          int64_t m, int64_t mp, bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
         for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < mp;
              c += (int64_t)gridDim.x * blockDim.x) {
@@ -87,6 +89,7 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
                                                               float *__restrict__ lo, int64_t m,
                                                               int64_t p, int64_t ldb, int64_t mp,
                                                               bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     __shared__ float tile[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t j0 = (int64_t)blockIdx.x * 32;  // column of B = row of Bt
@@ -113,6 +116,7 @@ __global__ void __launch_bounds__(256) split_transpose64_kernel(const float *__r
                                                                 float *__restrict__ lo, int64_t m,
                                                                 int64_t p, int64_t ldb, int64_t mp,
                                                                 bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     __shared__ float tile[64][65];
     const int tid = threadIdx.x;
     const int64_t j0 = (int64_t)blockIdx.x * 64;  // columns of B = rows of Bt
