@@ -124,7 +124,13 @@ la_status la_comm_init(const void *uid128, int rank, int ngpu) {
     // in flight (la_gemm_multi launches the GEMM on sms - reserved SMs).
     cfg.maxCTAs = reserved_sms() > 0 ? reserved_sms() : 8;
     cfg.minCTAs = 1;
-    LA_NCCL(ncclCommInitRankConfig(&g_comm.comm, ngpu, id, rank, &cfg));
+    ncclResult_t r = ncclCommInitRankConfig(&g_comm.comm, ngpu, id, rank, &cfg);
+    if (r == ncclInvalidArgument) {  // an NCCL that rejects the CTA bounds: default config
+        ncclConfig_t dflt = NCCL_CONFIG_INITIALIZER;
+        dflt.blocking = 1;
+        r = ncclCommInitRankConfig(&g_comm.comm, ngpu, id, rank, &dflt);
+    }
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRankConfig");
     g_comm.rank = rank;
     g_comm.size = ngpu;
     LA_CK(cudaStreamCreateWithFlags(&g_comm.stream, cudaStreamNonBlocking));
