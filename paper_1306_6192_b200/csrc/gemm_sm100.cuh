@@ -41,7 +41,8 @@
 
 namespace la {
 
-constexpr int BK = 32;            // K per stage: 32 fp32 = one 128-byte swizzle row
+constexpr int BK = 32;            // default K per stage: 32 fp32 = one 128-byte swizzle row
+                                  // (KB = 16: 64-byte rows, SWIZZLE_64B, twice the stages)
 constexpr int ROWS_PER_CTA = 128; // UMMA M per CTA
 constexpr int NUM_CTRL_WARPS = 4; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 tile scheduler
 constexpr int NUM_EPI_WARPS = 8;  // two per TMEM lane quarter (column halves)
@@ -146,13 +147,13 @@ struct SchedReader {
     }
 };
 
-template <int CG, int BN, int STAGES, int PASSES>
+template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 struct GemmCfg {
     static constexpr int TILE_M = CG * ROWS_PER_CTA;        // rows of C per tile
     static constexpr int B_ROWS = BN / CG;                  // rows of B^T staged per CTA
     static constexpr int NOPS = PASSES == 3 ? 2 : 1;        // hi (+ lo) tiles per operand
-    static constexpr int A_TILE = ROWS_PER_CTA * BK * 4;    // 16 KB
-    static constexpr int B_TILE = B_ROWS * BK * 4;
+    static constexpr int A_TILE = ROWS_PER_CTA * KB * 4;    // 16 KB at KB = 32
+    static constexpr int B_TILE = B_ROWS * KB * 4;
     static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);  // per CTA
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * 32 * 32 * 4; // per-warp transpose buffers
     static constexpr int BAR_BYTES = 512;  // mbarriers, TMEM address, tile ids; CLC response at +256
@@ -245,12 +246,12 @@ __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, u
     __syncwarp();
 }
 
-template <int CG, int BN, int STAGES, int PASSES>
+template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tf32_sm100_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                            const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                            const GemmArgs args) {
-    using Cfg = GemmCfg<CG, BN, STAGES, PASSES>;
+    using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // stage s: [A_hi | A_lo | B_hi | B_lo]   (identical offsets in both CTAs of a pair)
@@ -349,7 +350,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (lane == 0 && (args.debug & 1)) {
                     if (rank == 0) ptx::mbar_arrive(&full[s]);
                 } else if (lane == 0) {
-                    const int32_t k0 = kb * BK;
+                    const int32_t k0 = kb * KB;
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], CG * Cfg::STAGE_BYTES);
                     if constexpr (CG == 1) {
                         ptx::tma_load_2d(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
@@ -438,13 +439,13 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t al = ptx::smem_u32(a_tile(s, PASSES == 3 ? 1 : 0));
                     const uint32_t bl = ptx::smem_u32(b_tile(s, PASSES == 3 ? 1 : 0));
 #pragma unroll
-                    for (int j = 0; j < BK / 8; j++) {  // K = 8 per tf32 MMA = 32 bytes of a swizzled row
-                        const uint64_t dah = ptx::sdesc_kmajor_sw128(ah + 32 * j);
-                        const uint64_t dbh = ptx::sdesc_kmajor_sw128(bh + 32 * j);
+                    for (int j = 0; j < KB / 8; j++) {  // K = 8 per tf32 MMA = 32 bytes of a swizzled row
+                        const uint64_t dah = ptx::sdesc_kmajor<KB>(ah + 32 * j);
+                        const uint64_t dbh = ptx::sdesc_kmajor<KB>(bh + 32 * j);
                         const uint32_t acc = (chunk_first && j == 0) ? 0u : 1u;
                         if constexpr (PASSES == 3) {
-                            const uint64_t dal = ptx::sdesc_kmajor_sw128(al + 32 * j);
-                            const uint64_t dbl = ptx::sdesc_kmajor_sw128(bl + 32 * j);
+                            const uint64_t dal = ptx::sdesc_kmajor<KB>(al + 32 * j);
+                            const uint64_t dbl = ptx::sdesc_kmajor<KB>(bl + 32 * j);
                             ptx::mma_tf32<CG>(d, dah, dbl, idesc, acc);  // hi . lo'
                             ptx::mma_tf32<CG>(d, dal, dbh, idesc, 1u);   // lo . hi'
                             ptx::mma_tf32<CG>(d, dah, dbh, idesc, 1u);   // hi . hi'

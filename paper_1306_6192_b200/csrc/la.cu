@@ -65,15 +65,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
 // 2-D fp32 tensor map over a rows x cols row-major buffer (cols % 4 == 0),
 // box = box_rows x 32 columns, 128-byte swizzle, OOB elements read as zero.
 static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols,
-                           int box_rows) {
+                           int box_rows, int box_k = BK) {
     auto enc = get_encoder();
     if (!enc) return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};  // box_rows <= 256
+    cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)box_rows};  // box_rows <= 256
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld", (int)r,
@@ -209,18 +210,18 @@ static int splitk_factor(int64_t tiles, int64_t slots, int num_kb) {
     return (num_kb + per - 1) / per;
 }
 
-template <int CG, int BN, int STAGES, int PASSES>
+template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C,
                              int64_t ldc, int max_sms, cudaStream_t st, int *launches, const OutSpec &out) {
-    using Cfg = GemmCfg<CG, BN, STAGES, PASSES>;
+    using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB>;
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     la_status s;
     const float *bh = ops.b_hi + j0 * ops.mp, *bl = ops.b_lo + j0 * ops.mp;
-    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA)) != LA_OK) return s;
-    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS)) != LA_OK) return s;
+    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA, KB)) != LA_OK) return s;
+    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS, KB)) != LA_OK) return s;
     if (PASSES == 3) {
-        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, ROWS_PER_CTA)) != LA_OK) return s;
-        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, Cfg::B_ROWS)) != LA_OK) return s;
+        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, ROWS_PER_CTA, KB)) != LA_OK) return s;
+        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, Cfg::B_ROWS, KB)) != LA_OK) return s;
     } else {
         ta_lo = ta_hi;
         tb_lo = tb_hi;
@@ -238,11 +239,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.gather_row0 = out.gather_row0;
     args.gather_col0 = out.gather_col0 + j0;
     args.gather_ld = out.gather_ld;
-    args.num_kb = (int32_t)((m + BK - 1) / BK);
+    args.num_kb = (int32_t)((m + KB - 1) / KB);
     // Promotion only in 3xTF32: plain TF32's 2^-9 bound is 2^11 times looser than
     // the truncation bias of whole-K accumulation (~3 x 2^-20 S at K = 16384).
     const int64_t pk = PASSES == 3 ? g_state.promote_k : 0;
-    args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + BK - 1) / BK);
+    args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + KB - 1) / KB);
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
@@ -250,7 +251,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.group_m = group_env > 0 ? group_env : 8;
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
 
-    auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES>;
+    auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES, KB>;
     static int max_clusters = 0;
     if (max_clusters == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
@@ -300,7 +301,8 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.partial = nullptr;
     void *part_buf = nullptr;
     {
-        const int S = (out.splitk_ok && !args.use_clc) ? splitk_factor(tiles, max_clusters, args.num_kb) : 1;
+        const int kb32 = (int)((m + 31) / 32);
+        const int S = (out.splitk_ok && !args.use_clc) ? splitk_factor(tiles, max_clusters, kb32) : 1;
         if (S > 1) {
             // pieces of kb_per K-blocks; recount S from the piece size so every
             // piece is non-empty ((S - 1) * kb_per < num_kb)
@@ -355,7 +357,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     const char *ws_env = getenv("LA_WAVE_SYNC");
     // Never with an SM cap: the capped launch runs beside other kernels (NCCL in
     // la_gemm_multi) and every participant of a wave must be resident.
-    int wave_sync = ws_env ? atoi(ws_env) : (args.num_kb >= 64 ? 16 : 0);
+    int wave_sync = ws_env ? atoi(ws_env) * BK / KB : (args.num_kb * KB >= 64 * BK ? 16 * BK / KB : 0);
     if (max_sms > 0 || args.ksplit > 1) wave_sync = 0;
     if (!args.use_clc && wave_sync > 0) {
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
@@ -433,12 +435,14 @@ static int choose_cta_group(int64_t n, int64_t pc, int num_kb, bool splitk_ok) {
 
 la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C, int64_t ldc,
                    int max_sms, cudaStream_t st, int *launches, OutSpec out) {
-    const int num_kb = (int)((m + BK - 1) / BK);
+    const int num_kb = (int)((m + 31) / 32);  // cost model in 32-wide K-blocks
     const bool splitk_ok = out.splitk_ok && max_sms <= 0 && out.cstride == 1 && out.half_rows == 0 &&
                            out.gather_win == nullptr && ldc == pc;
     out.splitk_ok = splitk_ok;
     const int cg = choose_cta_group(n, pc, num_kb, splitk_ok);
+    const bool bk16 = getenv("LA_BK") && atoi(getenv("LA_BK")) == 16;  // A/B knob: 64-byte K rows, 6 stages
     if (ops.passes == 3) {
+        if (cg == 2 && bk16) return launch_gemm<2, 256, 6, 3, 16>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
     }

@@ -277,9 +277,20 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // atoms of 1024 B.  Fields: start>>4 [0,14), LBO>>4 [16,30) (unused for
 // swizzled K-major, 1), SBO>>4 [32,46) = 1024 B between 8-row groups,
 // version 1 at [46,48), layout type SWIZZLE_128B = 2 at [61,64).
+// Same for 64-byte rows (16 fp32 of K, SWIZZLE_64B = 4, 8-row atoms of 512 B).
+__device__ __forceinline__ uint64_t sdesc_kmajor_sw64(uint32_t smem_addr) {
+    return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
+           ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
 __device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t smem_addr) {
     return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
            ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+template <int KB>
+__device__ __forceinline__ uint64_t sdesc_kmajor(uint32_t smem_addr) {
+    if constexpr (KB == 32) return sdesc_kmajor_sw128(smem_addr);
+    else return sdesc_kmajor_sw64(smem_addr);
 }
 
 // Instruction descriptor, kind::tf32: D fp32 [4,6)=1, A tf32 [7,10)=2,
