@@ -344,6 +344,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
 #else
     args.debug = 0;
 #endif
+    args.prefetch = getenv("LA_PREFETCH") ? atoi(getenv("LA_PREFETCH")) : 0;  // A/B knob
     args.wave_sync = nullptr;
     args.sync_kb = args.num_kb;
     void *sync_buf = nullptr;
@@ -440,9 +441,9 @@ la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands 
                            out.gather_win == nullptr && ldc == pc;
     out.splitk_ok = splitk_ok;
     const int cg = choose_cta_group(n, pc, num_kb, splitk_ok);
-    const bool bk16 = getenv("LA_BK") && atoi(getenv("LA_BK")) == 16;  // A/B knob: 64-byte K rows, 6 stages
+    // (KB = 16 with a 6-stage ring was measured slower and costlier: 202 vs 244
+    // TFLOP/s and 42.9 vs 35.3 J per n = 16384 GEMM -- not dispatched.)
     if (ops.passes == 3) {
-        if (cg == 2 && bk16) return launch_gemm<2, 256, 6, 3, 16>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
     }
