@@ -86,7 +86,6 @@ struct GemmArgs {
                         // (wave, K phase of sync_kb K-blocks)
     int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
     int32_t debug;      // diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip MMAs
-    int32_t prefetch;   // > 0: also prefetch the operand tiles `prefetch` K-blocks ahead into L2
     // Fused all-gather (la_gemm_multi into a registered symmetric C_full): every
     // output element (r, c) is also stored at row gather_row0 + r, column
     // gather_col0 + c (row stride gather_ld) of each LSA peer's window, i.e.
@@ -353,15 +352,6 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 } else if (lane == 0) {
                     const int32_t k0 = kb * KB;
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], CG * Cfg::STAGE_BYTES);
-                    if (args.prefetch > 0 && kb + args.prefetch < kb1) {
-                        const int32_t kp = (kb + args.prefetch) * KB;
-                        ptx::tma_prefetch_2d(&tm_a_hi, kp, m0);
-                        ptx::tma_prefetch_2d(&tm_b_hi, kp, n0);
-                        if constexpr (PASSES == 3) {
-                            ptx::tma_prefetch_2d(&tm_a_lo, kp, m0);
-                            ptx::tma_prefetch_2d(&tm_b_lo, kp, n0);
-                        }
-                    }
                     if constexpr (CG == 1) {
                         ptx::tma_load_2d(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
                         ptx::tma_load_2d(b_tile(s, 0), &tm_b_hi, &full[s], k0, n0, pol);

@@ -344,7 +344,6 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
 #else
     args.debug = 0;
 #endif
-    args.prefetch = getenv("LA_PREFETCH") ? atoi(getenv("LA_PREFETCH")) : 0;  // A/B knob
     args.wave_sync = nullptr;
     args.sync_kb = args.num_kb;
     void *sync_buf = nullptr;
