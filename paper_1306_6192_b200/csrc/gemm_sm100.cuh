@@ -432,7 +432,9 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 }
                 ptx::mbar_wait(&full[s], ph);
                 ptx::tc_fence_after();
-                if (lane == 0) {
+                {
+                    // whole warp, converged: descriptors are warp-uniform; one
+                    // elected lane issues each MMA / commit (ptx::*_elect)
                     const uint32_t d = tmem_base + buf * BN;
                     if (!(args.debug & 2)) {
                     const uint32_t ah = ptx::smem_u32(a_tile(s, 0)), bh = ptx::smem_u32(b_tile(s, 0));
@@ -446,16 +448,16 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         if constexpr (PASSES == 3) {
                             const uint64_t dal = ptx::sdesc_kmajor<KB>(al + 32 * j);
                             const uint64_t dbl = ptx::sdesc_kmajor<KB>(bl + 32 * j);
-                            ptx::mma_tf32<CG>(d, dah, dbl, idesc, acc);  // hi . lo'
-                            ptx::mma_tf32<CG>(d, dal, dbh, idesc, 1u);   // lo . hi'
-                            ptx::mma_tf32<CG>(d, dah, dbh, idesc, 1u);   // hi . hi'
+                            ptx::mma_tf32_elect<CG>(d, dah, dbl, idesc, acc);  // hi . lo'
+                            ptx::mma_tf32_elect<CG>(d, dal, dbh, idesc, 1u);   // lo . hi'
+                            ptx::mma_tf32_elect<CG>(d, dah, dbh, idesc, 1u);   // hi . hi'
                         } else {
-                            ptx::mma_tf32<CG>(d, dah, dbh, idesc, acc);
+                            ptx::mma_tf32_elect<CG>(d, dah, dbh, idesc, acc);
                         }
                     }
                     }
-                    ptx::mma_commit<CG>(&empty[s]);
-                    if (chunk_last) ptx::mma_commit<CG>(&tfull[buf]);
+                    ptx::mma_commit_elect<CG>(&empty[s]);
+                    if (chunk_last) ptx::mma_commit_elect<CG>(&tfull[buf]);
                 }
                 __syncwarp();
                 if (chunk_last) {

@@ -236,6 +236,48 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// Warp-converged variants: every lane of the warp executes them with identical
+// (warp-uniform) operands, and one lane elected inside the asm issues the
+// instruction.  Keeping the whole warp converged lets ptxas hold descriptors in
+// uniform registers instead of wrapping each UTCHMMA in an ELECT/R2UR waterfall
+// loop (which made the single issuing thread the bottleneck at high clocks).
+template <int CG>
+__device__ __forceinline__ void mma_tf32_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    if constexpr (CG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+template <int CG>
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar, uint16_t cta_mask = 0x3) {
+    if constexpr (CG == 1)
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                smem_u32(bar))
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+            "h"(cta_mask)
+            : "memory");
+}
+
 // Arrive (once) on an mbarrier when all previously issued tcgen05 ops of this
 // thread complete.  CG==2: arrive on the barrier at the same offset in every
 // CTA of `cta_mask`.
