@@ -357,7 +357,10 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     const char *ws_env = getenv("LA_WAVE_SYNC");
     // Never with an SM cap: the capped launch runs beside other kernels (NCCL in
     // la_gemm_multi) and every participant of a wave must be resident.
-    int wave_sync = ws_env ? atoi(ws_env) * BK / KB : (args.num_kb * KB >= 64 * BK ? 16 * BK / KB : 0);
+    // Default only for 3xTF32: with one TF32 pass each K phase is 3x shorter and
+    // the barrier costs more than it saves (n = 8192 TF32: 660 vs 628 TFLOP/s off/on).
+    int wave_sync = ws_env ? atoi(ws_env) * BK / KB
+                           : (PASSES == 3 && args.num_kb * KB >= 64 * BK ? 16 * BK / KB : 0);
     if (max_sms > 0 || args.ksplit > 1) wave_sync = 0;
     if (!args.use_clc && wave_sync > 0) {
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
