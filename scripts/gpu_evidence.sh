@@ -11,3 +11,4 @@ A="--steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 300 python bench.py $A > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_tf32|split" --csv --log-file gpurun_out/launches.csv python bench.py $A > gpurun_out/ncu_list.log 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tf32 -s 1 -c 1 -o gpurun_out/gemm_full python bench.py $A > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 600 python scripts/mode_speed.py > gpurun_out/modes.txt 2>&1; echo "modes rc=$?"
