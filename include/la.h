@@ -114,9 +114,11 @@ LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, cons
 /* End-to-end variant on HOST buffers (the paper's host flow):
  * copies h_A and h_B to the device, computes, copies C back into h_C and
  * returns after everything completed.  The copies are pipelined with the
- * compute: B first, then A in row panels on a copy-in stream, each panel's
- * split + GEMM on `stream` as soon as it lands, each C panel copied back on a
- * copy-out stream while later panels compute.  Every element accumulates in
+ * compute (2-D schedule): A row panels and B column panels alternate on a
+ * copy-in stream; each panel, as it lands, is split and unlocks one rectangle
+ * of C (that panel against every panel of the other operand already present),
+ * computed by one GEMM launch on `stream` and copied back on a copy-out stream
+ * while later panels are in flight.  Every element accumulates in
  * la_gemm's order (bitwise identical to la_gemm whenever la_gemm does not split
  * K).  Host buffers may be pageable or pinned (only pinned buffers overlap).
  * Device staging is library-owned and reused.  Errors: as la_gemm. */

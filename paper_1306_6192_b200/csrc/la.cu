@@ -597,6 +597,45 @@ la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float
 // panel, splits the A rows and runs the GEMM on them as soon as they land; a
 // copy-out stream returns each C panel while later panels compute.  With
 // pinned host buffers the copies overlap compute in both directions.
+// Panels per operand for la_gemm_host's 2-D transfer schedule (LA_HOST_PANELS
+// overrides; measured in profiles/e2e_r01.md).
+// LA_HOST_TRACE=1: print the schedule's timeline (ms after the first copy
+// starts) to stderr -- a diagnostic for profiles/e2e_r01.md, off by default.
+struct HostTrace {
+    bool on = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    void mark(const std::string &label, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        marks.push_back({label, e});
+    }
+    void dump() {
+        if (!on || marks.empty()) return;
+        cudaDeviceSynchronize();
+        for (auto &m : marks) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[0].second, m.second);
+            fprintf(stderr, "la_host_trace %8.3f %s\n", ms, m.first.c_str());
+        }
+        for (auto &m : marks) cudaEventDestroy(m.second);
+        marks.clear();
+    }
+};
+
+static int64_t host_tail_split() {
+    const char *v = getenv("LA_HOST_TAIL_SPLIT");
+    const int64_t t = v ? atoll(v) : 2;
+    return std::max<int64_t>(1, std::min<int64_t>(t, 16));
+}
+
+static int64_t host_panels() {
+    const char *v = getenv("LA_HOST_PANELS");
+    const int64_t q = v ? atoll(v) : 12;
+    return std::max<int64_t>(1, std::min<int64_t>(q, 64));
+}
+
 la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
                        void *stream) {
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
@@ -628,16 +667,34 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     float *dB = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256);
     float *dC = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256 + (bb + 255) / 256 * 256);
 
-    // row panels: 8 for big problems (multiples of the 256-row tile), else 1
-    const int64_t panel_rows = n >= 2048 ? ((n + 7) / 8 + 255) / 256 * 256 : n;
-    const int64_t P = (n + panel_rows - 1) / panel_rows;
-    while ((int64_t)g_state.host_events.size() < 2 * P + 2) {
+    // 2-D transfer schedule: A in row panels, B in column panels (widths and
+    // heights multiples of the 256-wide tile), interleaved on the copy-in stream
+    // so that the fraction of A and of B on the device grow together.  Each
+    // panel that lands unlocks one rectangle of C -- its rows (or columns)
+    // against every panel of the other operand already present -- computed by
+    // one GEMM launch and copied out while later panels are still in flight.
+    // Every C element is produced by exactly one tile over the whole K range, in
+    // la_gemm's order.
+    const int64_t q = host_panels();
+    auto panel = [q](int64_t len) {
+        return len >= 2048 ? std::min(len, ((len + q - 1) / q + 255) / 256 * 256) : len;
+    };
+    const int64_t rh = panel(n), pw = panel(p);
+    const int64_t Qr = (n + rh - 1) / rh, Qc = (p + pw - 1) / pw;
+    const int64_t tail_split = host_tail_split();
+    while ((int64_t)g_state.host_events.size() < 1 + 2 * (Qr + Qc) + 2 * tail_split) {
         cudaEvent_t e;
         LA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         g_state.host_events.push_back(e);
     }
-    cudaEvent_t ev_start = g_state.host_events[0], ev_b = g_state.host_events[1];
-    cudaEvent_t *ev_a = &g_state.host_events[2], *ev_c = &g_state.host_events[2 + P];
+    cudaEvent_t ev_start = g_state.host_events[0];
+    cudaEvent_t *ev_a = &g_state.host_events[1], *ev_b = ev_a + Qr, *ev_c = ev_b + Qc;
+    // arrival order: the operand whose present fraction is smaller goes next (A first)
+    std::vector<std::pair<bool, int64_t>> order;  // (is_A, panel index)
+    for (int64_t a = 0, bq = 0; a < Qr || bq < Qc;) {
+        if (bq >= Qc || (a < Qr && a * Qc <= bq * Qr)) order.push_back({true, a++});
+        else order.push_back({false, bq++});
+    }
 
     const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
     void *ws = nullptr;
@@ -649,33 +706,78 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     const Operands ops = operands_carve(ws, n, m, p, passes);
     int launches = 0;
 
-    // the copy-in stream starts after everything already queued on `st`
+    HostTrace tr;
+    tr.on = getenv("LA_HOST_TRACE") && atoi(getenv("LA_HOST_TRACE")) != 0;
+    // the copy streams start after everything already queued on `st`
     LA_CK(cudaEventRecord(ev_start, st));
     LA_CK(cudaStreamWaitEvent(g_state.h2d, ev_start, 0));
     LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_start, 0));
-    LA_CK(cudaMemcpyAsync(dB, h_B, bb, cudaMemcpyHostToDevice, g_state.h2d));
-    LA_CK(cudaEventRecord(ev_b, g_state.h2d));
-    for (int64_t i = 0; i < P; i++) {
-        const int64_t r0 = i * panel_rows, rows = std::min(panel_rows, n - r0);
-        LA_CK(cudaMemcpyAsync(dA + r0 * m, h_A + r0 * m, (size_t)(rows * m) * 4, cudaMemcpyHostToDevice,
-                              g_state.h2d));
-        LA_CK(cudaEventRecord(ev_a[i], g_state.h2d));
+    tr.mark("start", g_state.h2d);
+    for (const auto &o : order) {
+        if (o.first) {
+            const int64_t r0 = o.second * rh, rows = std::min(rh, n - r0);
+            LA_CK(cudaMemcpyAsync(dA + r0 * m, h_A + r0 * m, (size_t)(rows * m) * 4, cudaMemcpyHostToDevice,
+                                  g_state.h2d));
+            LA_CK(cudaEventRecord(ev_a[o.second], g_state.h2d));
+            tr.mark("h2d A" + std::to_string(o.second), g_state.h2d);
+        } else {
+            const int64_t c0 = o.second * pw, w = std::min(pw, p - c0);
+            LA_CK(cudaMemcpy2DAsync(dB + c0, (size_t)p * 4, h_B + c0, (size_t)p * 4, (size_t)w * 4, (size_t)m,
+                                    cudaMemcpyHostToDevice, g_state.h2d));
+            LA_CK(cudaEventRecord(ev_b[o.second], g_state.h2d));
+            tr.mark("h2d B" + std::to_string(o.second), g_state.h2d);
+        }
     }
-    LA_CK(cudaStreamWaitEvent(st, ev_b, 0));
-    la_status s = split_b(m, 0, p, dB, p, ops, st, &launches);
-    for (int64_t i = 0; i < P && s == LA_OK; i++) {
-        const int64_t r0 = i * panel_rows, rows = std::min(panel_rows, n - r0);
-        LA_CK(cudaStreamWaitEvent(st, ev_a[i], 0));
-        Operands pan = ops;
-        pan.a_hi = ops.a_hi + r0 * ops.mp;
-        pan.a_lo = ops.a_lo + r0 * ops.mp;
-        s = split_a(rows, m, dA + r0 * m, pan, st, &launches);
-        if (s == LA_OK) s = gemm_run(rows, m, 0, p, pan, dC + r0 * p, p, (int)g_state.max_sms, st, &launches);
-        if (s == LA_OK) {
-            LA_CK(cudaEventRecord(ev_c[i], st));
-            LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_c[i], 0));
-            LA_CK(cudaMemcpyAsync(h_C + r0 * p, dC + r0 * p, (size_t)(rows * p) * 4, cudaMemcpyDeviceToHost,
-                                  g_state.d2h));
+    la_status s = LA_OK;
+    int64_t rows_in = 0, cols_in = 0, regions = 0;
+    for (const auto &o : order) {
+        int64_t r0, r1, c0, c1;
+        if (o.first) {
+            r0 = o.second * rh;
+            r1 = std::min(n, r0 + rh);
+            LA_CK(cudaStreamWaitEvent(st, ev_a[o.second], 0));
+            Operands pan = ops;
+            pan.a_hi = ops.a_hi + r0 * ops.mp;
+            pan.a_lo = ops.a_lo + r0 * ops.mp;
+            s = split_a(r1 - r0, m, dA + r0 * m, pan, st, &launches);
+            rows_in = r1;
+            c0 = 0;
+            c1 = cols_in;
+        } else {
+            c0 = o.second * pw;
+            c1 = std::min(p, c0 + pw);
+            LA_CK(cudaStreamWaitEvent(st, ev_b[o.second], 0));
+            s = split_b(m, c0, c1 - c0, dB + c0, p, ops, st, &launches);
+            cols_in = c1;
+            r0 = 0;
+            r1 = rows_in;
+        }
+        if (s != LA_OK) break;
+        tr.mark(std::string("split ") + (o.first ? "A" : "B") + std::to_string(o.second), st);
+        if (r1 <= r0 || c1 <= c0) continue;
+        // the last two rectangles are computed in pieces along their long side
+        // so that the copy-out of one piece overlaps the GEMM of the next
+        const int64_t pieces = (int64_t)(&o - order.data()) + 2 >= (int64_t)order.size() ? tail_split : 1;
+        const bool by_rows = r1 - r0 >= c1 - c0;
+        const int64_t len = by_rows ? r1 - r0 : c1 - c0;
+        const int64_t step = std::max<int64_t>(256, ((len + pieces - 1) / pieces + 255) / 256 * 256);
+        for (int64_t x0 = 0; x0 < len && s == LA_OK; x0 += step) {
+            const int64_t x1 = std::min(len, x0 + step);
+            const int64_t q0 = by_rows ? r0 + x0 : r0, q1 = by_rows ? r0 + x1 : r1;
+            const int64_t k0 = by_rows ? c0 : c0 + x0, k1 = by_rows ? c1 : c0 + x1;
+            Operands pan = ops;
+            pan.a_hi = ops.a_hi + q0 * ops.mp;
+            pan.a_lo = ops.a_lo + q0 * ops.mp;
+            s = gemm_run(q1 - q0, m, k0, k1 - k0, pan, dC + q0 * p, p, (int)g_state.max_sms, st, &launches);
+            if (s != LA_OK) break;
+            tr.mark("gemm " + std::to_string(q1 - q0) + "x" + std::to_string(k1 - k0), st);
+            LA_CK(cudaEventRecord(ev_c[regions], st));
+            LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_c[regions], 0));
+            LA_CK(cudaMemcpy2DAsync(h_C + q0 * p + k0, (size_t)p * 4, dC + q0 * p + k0, (size_t)p * 4,
+                                    (size_t)(k1 - k0) * 4, (size_t)(q1 - q0), cudaMemcpyDeviceToHost,
+                                    g_state.d2h));
+            tr.mark("d2h " + std::to_string(regions), g_state.d2h);
+            regions++;
         }
     }
     cudaFreeAsync(ws, st);
@@ -687,6 +789,7 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     }
     LA_CK(cudaStreamSynchronize(g_state.d2h));
     LA_CK(cudaStreamSynchronize(st));
+    tr.dump();
     return LA_OK;
 }
 

@@ -162,11 +162,16 @@ def test_host_entry_point(la):
     assert np.array_equal(Cp.numpy(), C)
 
 
-@pytest.mark.parametrize("n,m,p", [(2300, 700, 900), (4096, 1024, 2048)])
-def test_host_entry_point_pipelined_panels(la, n, m, p, monkeypatch):
-    """n >= 2048 takes the pipelined row-panel path (ragged last panel at 2300);
-    bitwise equal to la_gemm without split-K (panels never split K)."""
+@pytest.mark.parametrize("n,m,p,q", [(2300, 700, 900, 16), (4096, 1024, 2048, 16), (2300, 700, 2900, 16),
+                                     (3000, 513, 2049, 3), (2048, 300, 6000, 8), (5000, 64, 2100, 64),
+                                     (4096, 1024, 4096, 1)])
+def test_host_entry_point_pipelined_panels(la, n, m, p, q, monkeypatch):
+    """Dimensions >= 2048 take the 2-D panel schedule (A row panels, B column
+    panels, one GEMM per unlocked rectangle; ragged last panels, odd p, unequal
+    panel counts); bitwise equal to la_gemm without split-K (rectangles never
+    split K)."""
     monkeypatch.setenv("LA_SPLIT_K", "0")
+    monkeypatch.setenv("LA_HOST_PANELS", str(q))
     A, B = inputs.pair(n, m, p, "stress", device="cuda")
     ref = la.gemm(A, B).cpu()
     Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
