@@ -371,9 +371,22 @@ def run_ours(a, rank, world, local_rank):
         "pct_tf32_datasheet": 100.0 * passes * flops / (ms * 1e-3) / 1e12 / TF32_DATASHEET_TFLOPS,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": launches, "parity_sample_max_err_units_2^-20": parity,
+        "paper_context": PAPER_CONTEXT,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# The paper's own figures (Table 2, 4096^3 fp32 product, wall seconds; GFLOP/s
+# derived as 2n^3/t): context for the line above, other hardware, not a target.
+PAPER_CONTEXT = [
+    {"hardware": "NVIDIA Tesla C1060 (30 SM x 8 SP)", "kernel": "Listing 3 (global memory)",
+     "workload": "4096^3 fp32", "time_s": 5.81, "gflops_derived": 23.7, "source": "PAPER.md:226, Table 2"},
+    {"hardware": "NVIDIA Tesla C2050", "kernel": "Listing 4 (16x16 shared-memory tiles)",
+     "workload": "4096^3 fp32", "time_s": 0.83, "gflops_derived": 165.6, "source": "PAPER.md:228, Table 2"},
+    {"hardware": "Intel Xeon E7-4860", "kernel": "Listing 1 (sequential loop)",
+     "workload": "4096^3 fp32", "time_s": 991.96, "gflops_derived": 0.139, "source": "PAPER.md:223, Table 2"},
+]
 
 
 def main():

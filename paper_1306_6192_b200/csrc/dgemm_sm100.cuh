@@ -17,6 +17,8 @@
 #pragma once
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace la {
 
 constexpr int DBM = 128, DBN = 128, DBK = 32, DSTAGES = 3;
@@ -158,6 +160,155 @@ __global__ void __launch_bounds__(DTHREADS, 1)
 #pragma unroll
             for (int ni = 0; ni < 4; ni++) {
                 const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t;
+                const double v0 = acc[mi][ni][2 * half], v1 = acc[mi][ni][2 * half + 1];
+                if (pair_ok && col + 1 < p) {
+                    *reinterpret_cast<double2 *>(crow + col) = make_double2(v0, v1);
+                } else {
+                    if (col < p) crow[col] = v0;
+                    if (col + 1 < p) crow[col + 1] = v1;
+                }
+            }
+        }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised TMA variant (m, p even; A, B 16-byte aligned).  The
+// cp.async kernel above leaves the DMMA pipe idle ~11% of the time (ncu: the
+// consumer warps also run the copy address arithmetic and a CTA-wide barrier
+// per K-stage).  Here one producer warp feeds a 3-stage ring with TMA
+// (SWIZZLE_128B boxes of 16 doubles, zero fill past every edge) and mbarriers;
+// the eight consumer warps only load fragments and issue DMMA.
+//
+// Shared layout per stage: A = 2 boxes (K halves) of 128 rows x 16 doubles,
+// B = 8 boxes (16-column groups) of 32 K-rows x 16 doubles; in each 128-byte
+// box row the 16-byte chunk c sits at chunk c ^ (row % 8).  Bank conflicts of
+// the fragment loads are removed by feeding the MMA's k index t (and t + 4) from
+// K-row sigma(t) = (t >> 1) | ((t & 1) << 2) (and sigma(t) + 2) of each 8-wide
+// K group -- the same permutation for A and B, so every product a_ik * b_kj is
+// still formed exactly once (only the order of the fp64 additions inside one
+// K group changes, which the binary64 bound already covers).
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+
+constexpr int DT_STAGES = 3;
+constexpr int DT_A_BYTES = DBM * DBK * 8;  // 32 KB
+constexpr int DT_B_BYTES = DBK * DBN * 8;  // 32 KB
+constexpr int DT_STAGE_BYTES = DT_A_BYTES + DT_B_BYTES;
+constexpr int DT_THREADS = 384;  // 2 consumer warpgroups + 1 producer warpgroup (one TMA lane)
+constexpr int DT_SMEM_BYTES = 1024 + DT_STAGES * DT_STAGE_BYTES + 2 * DT_STAGES * 8;
+// setmaxnreg: the pool is 384 x 168; the producer warpgroup shrinks to 40 so the
+// consumers (128 fp64 accumulators + fragments each) can grow to 232.
+constexpr int DT_LAUNCH_REGS = 168, DT_PROD_REGS = 40, DT_CONS_REGS = 232;
+static_assert(128 * DT_PROD_REGS + 256 * DT_CONS_REGS <= DT_THREADS * DT_LAUNCH_REGS, "register pool");
+
+__global__ void __launch_bounds__(DT_THREADS, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                     double *__restrict__ C, int64_t n, int64_t m, int64_t p) {
+    extern __shared__ __align__(1024) uint8_t dt_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(dt_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + DT_STAGES * DT_STAGE_BYTES);
+    uint64_t *empty = full + DT_STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t m0 = (int32_t)blockIdx.y * DBM, n0 = (int32_t)blockIdx.x * DBN;
+    const int kt_count = (int)((m + DBK - 1) / DBK);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < DT_STAGES; s++) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 8);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp >= 8) {  // producer warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(DT_PROD_REGS));
+        if (warp == 8 && lane == 0) {
+            ptx::prefetch_tmap(&tA);
+            ptx::prefetch_tmap(&tB);
+            const uint64_t pol = ptx::policy_evict_normal();
+            for (int kt = 0; kt < kt_count; kt++) {
+                const int s = kt % DT_STAGES;
+                ptx::mbar_wait(&empty[s], ((kt / DT_STAGES) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[s], DT_STAGE_BYTES);
+                uint8_t *a = smem + s * DT_STAGE_BYTES, *b = a + DT_A_BYTES;
+                const int32_t k0 = kt * DBK;
+                ptx::tma_load_2d(a, &tA, &full[s], k0, m0, pol);
+                ptx::tma_load_2d(a + DBM * 128, &tA, &full[s], k0 + 16, m0, pol);
+#pragma unroll
+                for (int j = 0; j < DBN / 16; j++) ptx::tma_load_2d(b + j * DBK * 128, &tB, &full[s], n0 + 16 * j, k0, pol);
+            }
+        }
+        return;
+    }
+
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(DT_CONS_REGS));
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp >> 2, wn = warp & 3;  // warp tile origin: rows wm*64, cols wn*32
+    const uint32_t sbase = ptx::smem_u32(smem);
+    const int s0 = (t >> 1) | ((t & 1) << 2), s1 = s0 + 2;  // K rows of MMA k = t, t + 4
+    // byte offsets inside a box (row term + swizzled chunk + 8-byte half)
+    const uint32_t a_lo = g * 128 + ((((uint32_t)s0 >> 1) ^ g) << 4) + (s0 & 1) * 8;
+    const uint32_t a_hi = g * 128 + ((((uint32_t)s1 >> 1) ^ g) << 4) + (s1 & 1) * 8;
+    const uint32_t b_lo = s0 * 128 + ((((uint32_t)g >> 1) ^ s0) << 4) + (g & 1) * 8;
+    const uint32_t b_hi = s1 * 128 + ((((uint32_t)g >> 1) ^ s1) << 4) + (g & 1) * 8;
+
+    double acc[4][4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int v = 0; v < 4; v++) acc[i][j][v] = 0.0;
+
+    for (int kt = 0; kt < kt_count; kt++) {
+        const int s = kt % DT_STAGES;
+        ptx::mbar_wait(&full[s], (kt / DT_STAGES) & 1);
+        const uint32_t as = sbase + s * DT_STAGE_BYTES + (wm * 64) * 128;
+        const uint32_t bs = sbase + s * DT_STAGE_BYTES + DT_A_BYTES + (wn * 2) * DBK * 128;
+#pragma unroll
+        for (int kk = 0; kk < DBK; kk += 8) {
+            const uint32_t xa = ((kk >> 3) & 1) << 6;  // chunk ^ 4 in the upper half of a box
+            const uint32_t ak = as + (kk >> 4) * (DBM * 128);
+            const uint32_t bk = bs + kk * 128;
+            double af[4][4], bf[4][2];
+#pragma unroll
+            for (int mi = 0; mi < 4; mi++) {
+                const uint32_t r = ak + mi * 16 * 128;
+                af[mi][0] = lds_f64(r + (a_lo ^ xa));
+                af[mi][1] = lds_f64(r + 1024 + (a_lo ^ xa));
+                af[mi][2] = lds_f64(r + (a_hi ^ xa));
+                af[mi][3] = lds_f64(r + 1024 + (a_hi ^ xa));
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ni++) {
+                const uint32_t xb = (ni & 1) << 6;
+                const uint32_t c = bk + (ni >> 1) * DBK * 128;
+                bf[ni][0] = lds_f64(c + (b_lo ^ xb));
+                bf[ni][1] = lds_f64(c + (b_hi ^ xb));
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+                for (int ni = 0; ni < 4; ni++) dmma_16x8x8(acc[mi][ni], af[mi], bf[ni]);
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    }
+
+    const bool pair_ok = (p & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+            const int64_t row = (int64_t)m0 + wm * 64 + mi * 16 + g + 8 * half;
+            if (row >= n) continue;
+            double *crow = C + row * p;
+#pragma unroll
+            for (int ni = 0; ni < 4; ni++) {
+                const int64_t col = (int64_t)n0 + wn * 32 + ni * 8 + 2 * t;
                 const double v0 = acc[mi][ni][2 * half], v1 = acc[mi][ni][2 * half + 1];
                 if (pair_ok && col + 1 < p) {
                     *reinterpret_cast<double2 *>(crow + col) = make_double2(v0, v1);

@@ -82,6 +82,24 @@ static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int
     return LA_OK;
 }
 
+// Row-major fp64 matrix (rows x cols) for the DGEMM's TMA boxes of 16 doubles x
+// box_rows, 128-byte swizzle.  cols must be even (16-byte row stride).
+static la_status make_tmap_f64(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int box_rows) {
+    auto enc = get_encoder();
+    if (!enc) return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(double)};
+    cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled (f64) failed (%d) rows=%lld cols=%lld", (int)r,
+                    (long long)rows, (long long)cols);
+    return LA_OK;
+}
+
 // ---- optional per-kernel device timing (bench.py roofline) ----------------
 struct TimedSpan {
     cudaEvent_t a, b;
@@ -884,11 +902,28 @@ la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const dou
     }
     const bool vec16 = m % 2 == 0 && p % 2 == 0 &&
                        ((reinterpret_cast<uintptr_t>(d_A) | reinterpret_cast<uintptr_t>(d_B)) & 15) == 0;
+    // TMA path (int32 box coordinates); LA_DGEMM_CPASYNC=1 selects the cp.async kernel (A/B knob)
+    const bool tma = vec16 && n < ((int64_t)1 << 31) && m < ((int64_t)1 << 31) && p < ((int64_t)1 << 31) &&
+                     !(getenv("LA_DGEMM_CPASYNC") && atoi(getenv("LA_DGEMM_CPASYNC")) != 0);
+    CUtensorMap tA, tB;
+    if (tma) {
+        static bool attr_tma = false;
+        if (!attr_tma) {
+            cudaError_t e = cudaFuncSetAttribute(dgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 DT_SMEM_BYTES);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(dgemm_tma)", __FILE__, __LINE__);
+            attr_tma = true;
+        }
+        la_status ms;
+        if ((ms = make_tmap_f64(&tA, d_A, n, m, DBM)) != LA_OK) return ms;
+        if ((ms = make_tmap_f64(&tB, d_B, m, p, DBK)) != LA_OK) return ms;
+    }
     cudaEvent_t t0;
     la_status s = timing_begin(st, &t0);
     if (s != LA_OK) return s;
     const dim3 grid((unsigned)gx, (unsigned)gy);
-    if (vec16) dgemm_sm100_kernel<true><<<grid, DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
+    if (tma) dgemm_tma_kernel<<<grid, DT_THREADS, DT_SMEM_BYTES, st>>>(tA, tB, d_C, n, m, p);
+    else if (vec16) dgemm_sm100_kernel<true><<<grid, DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
     else dgemm_sm100_kernel<false><<<grid, DTHREADS, DSMEM_BYTES, st>>>(d_A, d_B, d_C, n, m, p);
     g_state.last_launches = 1;
     cudaError_t e = cudaGetLastError();

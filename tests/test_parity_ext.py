@@ -113,12 +113,32 @@ def _dcheck(A, B, C, kind):
 
 @pytest.mark.parametrize("kind", ["integer", "f64"])
 @pytest.mark.parametrize("n,m,p", [(1, 1, 1), (5, 3, 7), (128, 16, 128), (129, 17, 131), (300, 1000, 257),
-                                   (1024, 1024, 1024)])
+                                   (1024, 1024, 1024), (2, 2, 2), (258, 66, 130), (1000, 2000, 1500),
+                                   (131, 34, 18)])
 def test_dgemm_parity(la, kind, n, m, p):
+    """Even m and p with 16-byte aligned operands take the TMA kernel (ragged
+    tiles in every dimension here), odd ones the cp.async kernel."""
     A = inputs.generate_f64(n, m, 0, kind)
     B = inputs.generate_f64(m, p, 1, kind)
     C = la.dgemm(A.cuda(), B.cuda()).cpu().numpy()
     _dcheck(A, B, C, kind)
+
+
+@pytest.mark.parametrize("n,m,p", [(256, 512, 256), (300, 1000, 258), (64, 4096, 130)])
+def test_dgemm_tma_and_cpasync_kernels_agree(la, n, m, p, monkeypatch):
+    """The TMA kernel (K permuted inside each 8-wide group) and the cp.async
+    kernel: identical on integer inputs, each within the binary64 bound."""
+    Ai = inputs.generate_f64(n, m, 0, "integer", device="cuda")
+    Bi = inputs.generate_f64(m, p, 1, "integer", device="cuda")
+    A = inputs.generate_f64(n, m, 0, device="cuda")
+    B = inputs.generate_f64(m, p, 1, device="cuda")
+    out = {}
+    for knob in ("0", "1"):
+        monkeypatch.setenv("LA_DGEMM_CPASYNC", knob)
+        out[knob] = (la.dgemm(Ai, Bi).cpu(), la.dgemm(A, B).cpu())
+    assert torch.equal(out["0"][0], out["1"][0])
+    for knob in ("0", "1"):
+        _dcheck(A.cpu(), B.cpu(), out[knob][1].numpy(), "f64")
 
 
 def test_dgemm_4096_sampled(la):
