@@ -1,0 +1,40 @@
+"""The C ABI from plain C: tests/c/abi_host.c includes only include/la.h,
+links libla.so and calls it with host buffers.  On CPU the program must
+compile warning-free as C99, link, and report the missing GPU (exit 77); on a
+B200 it must pass (exact integer product, error paths)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _build(tmp_path):
+    import paper_1306_6192_b200 as la
+    libdir = os.path.dirname(la.LIB_PATH)
+    exe = str(tmp_path / "abi_host")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-pedantic", "-O2",
+                    "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c", "abi_host.c"),
+                    "-o", exe, "-L", libdir, "-l:libla.so", f"-Wl,-rpath,{libdir}"], check=True)
+    return exe
+
+
+def _has_gpu():
+    import torch
+    return torch.cuda.is_available()
+
+
+def test_c_consumer_builds_and_reports_no_gpu(tmp_path):
+    if _has_gpu():
+        pytest.skip("a GPU is present; see test_c_consumer_on_gpu")
+    r = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 77, r.stdout + r.stderr
+    assert "la_init" in r.stderr
+
+
+@pytest.mark.gpu
+def test_c_consumer_on_gpu(tmp_path):
+    r = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "exact" in r.stdout
