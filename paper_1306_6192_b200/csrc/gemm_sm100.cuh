@@ -143,7 +143,7 @@ struct SchedReader {
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cta0<CG>(&sempty[slot]);
         if (++slot == SCHED_SLOTS) { slot = 0; ph ^= 1; }
-        return t;
+        return __shfl_sync(0xffffffffu, t, 0);  // warp-uniform for the compiler (uniform datapath)
     }
 };
 
@@ -310,7 +310,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
+    const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);  // uniform
 
     const int num_items = args.num_items;
     const int num_kb = args.num_kb;
