@@ -213,6 +213,35 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     return timing_end(st, t0, TIMED_SPLIT);
 }
 
+// Both splits in one launch when A takes the float4 pass and B the 64 x 64
+// vectorised transpose; returns false (nothing launched) otherwise.
+static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const Operands &ops,
+                     cudaStream_t st, int *launches, la_status *status) {
+    const bool t32 = getenv("LA_SPLIT_T32") && atoi(getenv("LA_SPLIT_T32")) != 0;
+    if (m % 4 || p % 4 || ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) || t32 ||
+        (getenv("LA_SPLIT_SEPARATE") && atoi(getenv("LA_SPLIT_SEPARATE")) != 0))
+        return false;
+    const int64_t count4 = n * m / 4;
+    const int64_t na = std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, (int64_t)g_state.sms * 8));
+    const int64_t nbx = (p + 63) / 64, nby = (ops.mp + 63) / 64;
+    if (na + nbx * nby > INT32_MAX) return false;
+    cudaEvent_t t0;
+    if ((*status = timing_begin(st, &t0)) != LA_OK) return true;
+    const unsigned grid = (unsigned)(na + nbx * nby);
+    const float4 *a4 = reinterpret_cast<const float4 *>(A);
+    float4 *ah = reinterpret_cast<float4 *>(ops.a_hi), *al = reinterpret_cast<float4 *>(ops.a_lo);
+    if (ops.passes == 3)
+        split_ab_kernel<3><<<grid, 256, 0, st>>>(a4, ah, al, count4, na, B, ops.b_hi, ops.b_lo, m, p, ops.mp, nbx,
+                                                 lo_raw());
+    else
+        split_ab_kernel<1><<<grid, 256, 0, st>>>(a4, ah, al, count4, na, B, ops.b_hi, ops.b_lo, m, p, ops.mp, nbx,
+                                                 lo_raw());
+    (*launches)++;
+    cudaError_t e = cudaGetLastError();
+    *status = e != cudaSuccess ? cuda_fail(e, "split_ab launch", __FILE__, __LINE__) : timing_end(st, t0, TIMED_SPLIT);
+    return true;
+}
+
 // Split-K factor for a launch of `tiles` output tiles over `slots` concurrent
 // clusters: only with few tiles (at most half the slots) and a long K, at least
 // 8 K-blocks per piece, at most 16 pieces.
@@ -501,8 +530,11 @@ static la_status gemm_impl(int64_t n, int64_t m, int64_t p, const float *A, cons
         return fail(LA_ERR_OUT_OF_MEMORY, "workspace of %zu bytes: %s", bytes, cudaGetErrorString(e));
     }
     const Operands ops = operands_carve(ws, n, m, p, passes);
-    la_status s = split_a(n, m, A, ops, st, launches);
-    if (s == LA_OK) s = split_b(m, 0, p, B, p, ops, st, launches);
+    la_status s = LA_OK;
+    if (!split_ab(n, m, p, A, B, ops, st, launches, &s)) {
+        s = split_a(n, m, A, ops, st, launches);
+        if (s == LA_OK) s = split_b(m, 0, p, B, p, ops, st, launches);
+    }
     OutSpec out;
     out.splitk_ok = true;
     if (s == LA_OK) s = gemm_run(n, m, 0, p, ops, C, ldc, (int)g_state.max_sms, st, launches, out);

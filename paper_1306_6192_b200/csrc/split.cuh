@@ -40,13 +40,10 @@ __device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64
 
 // Row-major A, m % 4 == 0: flat float4 grid-stride loop (mp == m).
 template <int PASSES>
-__global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__restrict__ a,
-                                                              float4 *__restrict__ hi,
-                                                              float4 *__restrict__ lo,
-                                                              int64_t count4, bool lo_raw) {
-    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
-         i += (int64_t)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void split_rows_vec4_body(const float4 *__restrict__ a, float4 *__restrict__ hi,
+                                                    float4 *__restrict__ lo, int64_t count4, int64_t block,
+                                                    int64_t nblocks, bool lo_raw) {
+    for (int64_t i = block * (int64_t)blockDim.x + threadIdx.x; i < count4; i += nblocks * blockDim.x) {
         const float4 x = __ldcs(a + i);
         float4 h, l;
         h.x = ptx::to_tf32_rna(x.x);
@@ -62,6 +59,15 @@ __global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__re
             __stcg(lo + i, l);
         }
     }
+}
+
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__restrict__ a,
+                                                              float4 *__restrict__ hi,
+                                                              float4 *__restrict__ lo,
+                                                              int64_t count4, bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
+    split_rows_vec4_body<PASSES>(a, hi, lo, count4, blockIdx.x, gridDim.x, lo_raw);
 }
 
 // Row-major A, general m: one block-row per grid.y step, columns padded to mp.
@@ -111,16 +117,13 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
 // Bt (p x mp): 64 x 64 tiles, 16-byte loads along j and 16-byte stores along k
 // (each half-warp writes 256 contiguous bytes of one Bt row).  Block 256.
 template <int PASSES>
-__global__ void __launch_bounds__(256) split_transpose64_kernel(const float *__restrict__ b,
-                                                                float *__restrict__ hi,
-                                                                float *__restrict__ lo, int64_t m,
-                                                                int64_t p, int64_t ldb, int64_t mp,
-                                                                bool lo_raw) {
-    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
-    __shared__ float tile[64][65];
+__device__ __forceinline__ void split_transpose64_body(const float *__restrict__ b, float *__restrict__ hi,
+                                                      float *__restrict__ lo, int64_t m, int64_t p, int64_t ldb,
+                                                      int64_t mp, int64_t bx, int64_t by, bool lo_raw,
+                                                      float (*tile)[65]) {
     const int tid = threadIdx.x;
-    const int64_t j0 = (int64_t)blockIdx.x * 64;  // columns of B = rows of Bt
-    const int64_t k0 = (int64_t)blockIdx.y * 64;  // rows of B = columns of Bt
+    const int64_t j0 = bx * 64;  // columns of B = rows of Bt
+    const int64_t k0 = by * 64;  // rows of B = columns of Bt
     // load: 64 rows (k) x 16 float4 (j); thread -> (row r = tid / 16 + 16 i, col4 c = tid % 16)
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -154,6 +157,37 @@ __global__ void __launch_bounds__(256) split_transpose64_kernel(const float *__r
             l.w = lo_part(x[3], h.w, lo_raw);
             __stcg(reinterpret_cast<float4 *>(lo + j * mp + k), l);
         }
+    }
+}
+
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_transpose64_kernel(const float *__restrict__ b,
+                                                                float *__restrict__ hi,
+                                                                float *__restrict__ lo, int64_t m,
+                                                                int64_t p, int64_t ldb, int64_t mp,
+                                                                bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
+    __shared__ float tile[64][65];
+    split_transpose64_body<PASSES>(b, hi, lo, m, p, ldb, mp, blockIdx.x, blockIdx.y, lo_raw, tile);
+}
+
+// Both operand splits of one la_gemm in ONE launch (saves a launch and the
+// first kernel's tail on small and mid-size problems): blocks [0, na) run the
+// A pass (m % 4 == 0), the rest one 64 x 64 B tile each (the vectorised
+// transpose's conditions).  Same per-element arithmetic as the two kernels.
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_ab_kernel(const float4 *__restrict__ a, float4 *__restrict__ ahi,
+                                                       float4 *__restrict__ alo, int64_t count4, int64_t na,
+                                                       const float *__restrict__ b, float *__restrict__ bhi,
+                                                       float *__restrict__ blo, int64_t m, int64_t p, int64_t mp,
+                                                       int64_t nbx, bool lo_raw) {
+    asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
+    __shared__ float tile[64][65];
+    if ((int64_t)blockIdx.x < na) {
+        split_rows_vec4_body<PASSES>(a, ahi, alo, count4, blockIdx.x, na, lo_raw);
+    } else {
+        const int64_t t = (int64_t)blockIdx.x - na;
+        split_transpose64_body<PASSES>(b, bhi, blo, m, p, p, mp, t % nbx, t / nbx, lo_raw, tile);
     }
 }
 

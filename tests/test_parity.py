@@ -131,9 +131,24 @@ def test_launch_count_and_stream(la):
     with torch.cuda.stream(s):
         C = la.gemm(A, B, stream=s)
     s.synchronize()
-    assert la.last_launch_count() == 3          # split A, split B, GEMM
+    assert la.last_launch_count() == 2          # fused split of A and B, GEMM
     ref = (A.cpu().double() @ B.cpu().double()).float()
     assert torch.equal(C.cpu(), ref)
+
+
+@pytest.mark.parametrize("n,m,p", [(256, 256, 256), (1000, 2000, 1500), (300, 516, 260), (130, 4, 64)])
+def test_fused_split_equals_separate_splits(la, n, m, p, monkeypatch):
+    """The one-launch split of A and B writes the same hi/lo as the two
+    separate kernels (bitwise equal products; 3 launches instead of 2)."""
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    fused = la.gemm(A, B)
+    assert la.last_launch_count() == 2
+    monkeypatch.setenv("LA_SPLIT_SEPARATE", "1")
+    sep = la.gemm(A, B)
+    assert la.last_launch_count() == 3
+    torch.cuda.synchronize()
+    assert torch.equal(fused, sep)
 
 
 def test_graph_capture(la):
@@ -274,7 +289,8 @@ def test_split_k_parity(la, n, m, p, monkeypatch):
     A, B = inputs.pair(n, m, p, "integer", device="cuda")
     rows = sorted({0, n // 3, n - 1})
     C = la.gemm(A, B)
-    assert la.last_launch_count() == 4          # split A, split B, GEMM, split-K reduction
+    fused = m % 4 == 0 and p % 4 == 0           # one launch splits A and B
+    assert la.last_launch_count() == (3 if fused else 4)  # split(s), GEMM, split-K reduction
     _check(A[rows].cpu().numpy(), B.cpu().numpy(), C[rows].cpu().numpy(), "integer", "3xtf32")
     A, B = inputs.pair(n, m, p, "stress", device="cuda")
     C1, C2 = la.gemm(A, B), la.gemm(A, B)
