@@ -25,6 +25,10 @@
  *    (or as LA_ERR_CUDA from a later la_* call).  la_gemm does no host
  *    synchronisation and allocates with cudaMallocAsync, so it may be captured
  *    into a CUDA graph.
+ *  - Library state is process-wide (one device per process, set by la_init).
+ *    Every entry point serialises its host-side work on one library lock, so
+ *    calls from several host threads are safe; their device work on different
+ *    streams may overlap.  la_gemm_host holds the lock until its copies finish.
  *  - Sizes are int64_t; all index arithmetic on the device is 64-bit
  *    (n*p = 2^32 at n = 65536 overflows Listing 4's 32-bit `int c`).
  *
@@ -85,7 +89,7 @@ typedef enum {
     LA_OPT_KERNEL_TIMING = 3
 } la_option;
 
-/* Bind the calling thread's library state to CUDA device `device`, check that it
+/* Bind the (process-wide) library state to CUDA device `device`, check that it
  * is compute capability 10.0 (sm_100, B200) and set up the workspace pool.
  * Idempotent for the same device.  Errors: INVALID_VALUE (no such device),
  * UNSUPPORTED (not sm_100), CUDA. */

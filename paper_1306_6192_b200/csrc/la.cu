@@ -1,9 +1,10 @@
 // la.cu -- host side of the C ABI declared in include/la.h (single-GPU path).
 //
 // la_gemm(n, m, p, A, B, C, stream) enqueues, on the caller's stream:
-//   1. K1 split of A  -> A_hi, A_lo   (n x mp, row-major, K-major for UMMA)
-//   2. K1 split of B  -> Bt_hi, Bt_lo (p x mp, B transposed to K-major)
-//   3. K2 persistent tcgen05 GEMM reading the four operands through TMA
+//   1. K1 split of A  -> A_hi, A_lo   (n x mp, row-major, K-major for UMMA) and
+//      split of B  -> Bt_hi, Bt_lo (p x mp, B transposed to K-major), one launch
+//      when both take the vectorised kernels (split_ab_kernel), else two
+//   2. K2 persistent tcgen05 GEMM reading the four operands through TMA
 // with the workspace taken from (and returned to) a CUDA memory pool in stream
 // order, so the call never synchronises the host and can be graph-captured.
 #include <cuda.h>
@@ -29,7 +30,7 @@ namespace la {
 
 thread_local std::string g_last_error;
 State g_state;
-std::mutex g_mutex;
+std::recursive_mutex g_mutex;  // serialises every entry point's host-side work
 
 la_status fail(la_status s, const char *fmt, ...) {
     char buf[512];
@@ -556,7 +557,7 @@ using namespace la;
 extern "C" {
 
 la_status la_init(int device) {
-    std::lock_guard<std::mutex> lk(g_mutex);
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     g_last_error.clear();
     if (g_state.initialized) {
         if (device == g_state.device) {
@@ -592,12 +593,14 @@ la_status la_init(int device) {
 }
 
 la_status la_set_mode(la_mode mode) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (mode != LA_MODE_3XTF32 && mode != LA_MODE_TF32) return fail(LA_ERR_INVALID_VALUE, "unknown mode %d", (int)mode);
     g_state.mode = mode;
     return LA_OK;
 }
 
 la_status la_set_option(la_option option, int64_t value) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     switch (option) {
         case LA_OPT_PROMOTE_K:
             if (value < 0) return fail(LA_ERR_INVALID_VALUE, "promote_k must be >= 0");
@@ -620,6 +623,7 @@ la_status la_set_option(la_option option, int64_t value) {
 }
 
 la_status la_get_option(la_option option, int64_t *value) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!value) return fail(LA_ERR_INVALID_VALUE, "NULL value pointer");
     switch (option) {
         case LA_OPT_PROMOTE_K: *value = g_state.promote_k; return LA_OK;
@@ -632,6 +636,7 @@ la_status la_get_option(la_option option, int64_t *value) {
 
 la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B, float *d_C,
                   void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     la_status s = validate_gemm(n, m, p, d_A, d_B, d_C);
     if (s != LA_OK) return s;
     int launches = 0;
@@ -688,6 +693,7 @@ static int64_t host_panels() {
 
 la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
                        void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
     if (!h_A || !h_B || !h_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
@@ -848,6 +854,7 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
 // one persistent GEMM launch writing interleaved complex64 C.
 la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const float *d_B, float *d_C,
                    void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
     if (2 * n > (int64_t)1 << 31 || 2 * m > (int64_t)1 << 31 || p > (int64_t)1 << 31)
@@ -908,6 +915,7 @@ la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const floa
 // Double-precision product (Table 2 "Double" column) on the DMMA path.
 la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const double *d_B, double *d_C,
                    void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
     if (!d_A || !d_B || !d_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
@@ -967,6 +975,7 @@ la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const dou
 // C may be exactly A or B (in place) but must not partially overlap them.
 la_status la_add(int64_t rows, int64_t cols, const float *d_A, const float *d_B, float *d_C, int subtract,
                  void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (rows <= 0 || cols <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
     if (!d_A || !d_B || !d_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
@@ -1010,7 +1019,7 @@ la_status la_shard_rows(int64_t n, int rank, int ngpu, int64_t *row0, int64_t *r
 }
 
 la_status la_finalize(void) {
-    std::lock_guard<std::mutex> lk(g_mutex);
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return LA_OK;
     cudaDeviceSynchronize();
     la_status s = comm_destroy();
@@ -1047,6 +1056,7 @@ const char *la_last_error(void) { return g_last_error.c_str(); }
 int la_last_launch_count(void) { return g_state.last_launches; }
 
 la_status la_kernel_times(double *split_ms, double *gemm_ms, int *gemm_launches) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!split_ms || !gemm_ms || !gemm_launches) return fail(LA_ERR_INVALID_VALUE, "NULL output pointer");
     double t[2] = {0.0, 0.0};
     int ng = 0;

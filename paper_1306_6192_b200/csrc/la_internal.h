@@ -37,7 +37,7 @@ la_status timing_begin(cudaStream_t st, cudaEvent_t *ev);
 la_status timing_end(cudaStream_t st, cudaEvent_t ev, TimedKind kind);
 
 extern State g_state;
-extern std::mutex g_mutex;
+extern std::recursive_mutex g_mutex;  // serialises every entry point's host-side work
 extern thread_local std::string g_last_error;
 
 la_status fail(la_status s, const char *fmt, ...);

@@ -100,6 +100,7 @@ using namespace la;
 extern "C" {
 
 la_status la_get_unique_id(void *out128) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!out128) return fail(LA_ERR_INVALID_VALUE, "NULL unique-id buffer");
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
     ncclUniqueId id;
@@ -109,6 +110,7 @@ la_status la_get_unique_id(void *out128) {
 }
 
 la_status la_comm_init(const void *uid128, int rank, int ngpu) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (!uid128 || ngpu < 1 || rank < 0 || rank >= ngpu)
         return fail(LA_ERR_INVALID_VALUE, "bad communicator arguments rank=%d ngpu=%d", rank, ngpu);
@@ -139,6 +141,7 @@ la_status la_comm_init(const void *uid128, int rank, int ngpu) {
 }
 
 la_status la_gather_alloc(int64_t bytes, void **d_out) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (!g_comm.comm) return fail(LA_ERR_NOT_INITIALIZED, "la_comm_init has not been called");
     if (bytes <= 0 || !d_out) return fail(LA_ERR_INVALID_VALUE, "bad gather buffer request");
@@ -164,6 +167,7 @@ la_status la_gather_alloc(int64_t bytes, void **d_out) {
 
 la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local, const float *d_B,
                         float *d_C_local, float *d_C_full, int root, int ngpu, void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
     if (!g_comm.comm) return fail(LA_ERR_NOT_INITIALIZED, "la_comm_init has not been called");
     if (ngpu != g_comm.size)

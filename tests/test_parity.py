@@ -337,3 +337,36 @@ def test_split_k_forced_factors(la, forced, monkeypatch):
     C = la.gemm(A, B)
     rows = [0, 101, 199]
     _check(A[rows].cpu().numpy(), B.cpu().numpy(), C[rows].cpu().numpy(), "integer", "3xtf32")
+
+
+def test_concurrent_host_threads(la):
+    """Entry points called from several host threads at once (ctypes releases
+    the GIL): each thread on its own stream, plus la_gemm_host; all exact."""
+    import threading
+    A, B = inputs.pair(384, 520, 264, "integer", device="cuda")
+    ref = la.gemm(A, B).cpu()
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    errors = []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            outs = []
+            with torch.cuda.stream(s):
+                for _ in range(10):
+                    outs.append(la.gemm(A, B, stream=s))
+            s.synchronize()
+            for C in outs:
+                if not torch.equal(C.cpu(), ref):
+                    errors.append(f"thread {k}: la_gemm mismatch")
+            if k % 2 == 0 and not np.array_equal(la.gemm_host(Ah, Bh), ref.numpy()):
+                errors.append(f"thread {k}: la_gemm_host mismatch")
+        except Exception as ex:  # surfaced below
+            errors.append(f"thread {k}: {ex!r}")
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
