@@ -334,6 +334,10 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     const bool env_clc = getenv("LA_CLC") && atoi(getenv("LA_CLC")) != 0;
     args.use_clc = (max_sms <= 0 && env_clc) ? 1 : 0;
     if (max_sms > 0) clusters = std::min(clusters, std::max(1, max_sms / CG));
+#ifdef LA_DIAGNOSTICS
+    // energy diagnostics: fewer resident clusters with the wave barrier kept
+    if (const char *mc = getenv("LA_DIAG_CLUSTERS")) clusters = std::min(clusters, std::max(1, atoi(mc)));
+#endif
     clusters = (int)std::min<int64_t>(tiles, clusters);
     if (args.use_clc) {
         if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
