@@ -109,11 +109,30 @@ static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *
     }
 }
 
-// Optional K-phase alignment of the static persistent schedule: before the
-// first load of its w-th tile every producer arrives on counter w and waits
-// (bounded, 200 us) until all producers of that wave have arrived, so the
-// clusters that share A rows / B columns stream through K together and reuse
-// each other's slabs in L2 instead of re-reading them from HBM.
+// Same, four elements per thread (count % 4 == 0, 16-byte aligned buffers).
+static __global__ void __launch_bounds__(256) splitk_reduce_vec4_kernel(const float4 *__restrict__ part,
+                                                                 float4 *__restrict__ C, int64_t count4,
+                                                                 int ksplit) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 acc = __ldcs(part + i);
+        for (int s = 1; s < ksplit; s++) {
+            const float4 v = __ldcs(part + (int64_t)s * count4 + i);
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        C[i] = acc;
+    }
+}
+
+// Optional K-phase alignment of the static persistent schedule: at every K
+// phase of sync_kb K-blocks each producer of a wave arrives on that (wave,
+// phase) counter and waits (bounded, 200 us) until all producers of the wave
+// have arrived, so the clusters that share A rows / B columns stream through K
+// together and reuse each other's slabs in L2 instead of re-reading them from
+// HBM.
 __device__ __forceinline__ void wave_barrier(int32_t *ctr, int target) {
     atomicAdd(ctr, 1);
     uint64_t t0;

@@ -449,10 +449,16 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     if (rs != LA_OK) return rs;
     if (args.ksplit > 1) {
         const int64_t count = n * pc;
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)g_state.sms * 8));
+        const bool vec = count % 4 == 0 && (reinterpret_cast<uintptr_t>(args.C) & 15) == 0;
+        const int64_t work = vec ? count / 4 : count;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)g_state.sms * 8));
         cudaEvent_t t1;
         if ((rs = timing_begin(st, &t1)) != LA_OK) return rs;
-        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(args.partial, args.C, count, args.ksplit);
+        if (vec)
+            splitk_reduce_vec4_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(args.partial),
+                                                              reinterpret_cast<float4 *>(args.C), work, args.ksplit);
+        else
+            splitk_reduce_kernel<<<blocks, 256, 0, st>>>(args.partial, args.C, count, args.ksplit);
         (*launches)++;
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "split-K reduce launch", __FILE__, __LINE__);
