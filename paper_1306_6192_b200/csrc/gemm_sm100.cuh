@@ -86,6 +86,11 @@ struct GemmArgs {
                         // (wave, K phase of sync_kb K-blocks)
     int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
     int32_t debug;      // diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip MMAs
+    int64_t *trace;     // diagnostics only: per-CTA globaltimer stamps (8 per CTA), or nullptr
+    // 1: plain row-major output (cstride 1, no half rows, no gather) stored by
+    // TMA through the kernel's tm_c map {p, n, ksplit} (C, or the split-K
+    // partial slices); 0: per-thread stores (store_piece)
+    int32_t tma_store;
     // Fused all-gather (la_gemm_multi into a registered symmetric C_full): every
     // output element (r, c) is also stored at row gather_row0 + r, column
     // gather_col0 + c (row stride gather_ld) of each LSA peer's window, i.e.
@@ -107,6 +112,13 @@ static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *
         for (int s = 1; s < ksplit; s++) acc += part[(int64_t)s * count + i];
         C[i] = acc;
     }
+}
+
+__device__ __forceinline__ void trace_stamp(int64_t *trace, int k) {
+    if (trace == nullptr) return;
+    int64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    trace[blockIdx.x * 8 + k] = t;
 }
 
 // Same, four elements per thread (count % 4 == 0, 16-byte aligned buffers).
@@ -231,6 +243,30 @@ __device__ __forceinline__ float *row_ptr(const GemmArgs &args, int64_t r) {
     return args.C + r * args.ldc;
 }
 
+// The same 32 x 32 piece (row lane of the piece in v[0..31]) written by TMA:
+// the warp lays it out in its 4 KB smem buffer in the 128-byte-swizzle pattern
+// of tm_c (16-byte chunk j of row r at chunk j ^ (r % 8)), one lane issues the
+// bulk tensor store at (col0, row0, slice) and rows / columns past the map's
+// extent are clipped by the hardware.  The buffer is reused only after the
+// previous store has read it.
+__device__ __forceinline__ void store_piece_tma(const CUtensorMap *tm_c, float *tbuf, uint32_t lane, int64_t row0,
+                                                int64_t col0, int32_t slice, const uint32_t (&v)[32]) {
+    if (lane == 0) ptx::bulk_wait_read();
+    __syncwarp();
+    uint8_t *rowp = reinterpret_cast<uint8_t *>(tbuf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint4 w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        *reinterpret_cast<uint4 *>(rowp + ((j ^ (lane & 7)) << 4)) = w;
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        ptx::tma_store_3d(tm_c, tbuf, (int32_t)col0, (int32_t)row0, slice);
+        ptx::bulk_commit();
+    }
+}
+
 __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, uint32_t lane, int64_t row0,
                                             int64_t col0, const uint32_t (&v)[32],
                                             float *const *gbase = nullptr, float *cbase = nullptr) {
@@ -269,7 +305,7 @@ template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tf32_sm100_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                            const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
-                           const GemmArgs args) {
+                           const __grid_constant__ CUtensorMap tm_c, const GemmArgs args) {
     using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -293,6 +329,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) trace_stamp(args.trace, 0);
     const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;  // CTA rank in the pair
     const int cluster_id = blockIdx.x / CG;
     const int num_clusters = gridDim.x / CG;
@@ -328,6 +365,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_holder, Cfg::TMEM_COLS);
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (threadIdx.x == 0) trace_stamp(args.trace, 1);
     ptx::tc_fence_after();
     const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);  // uniform
 
@@ -345,6 +383,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         // allocation, tensor-map prefetch, cluster sync) overlapped the split
         // kernels' tail; the operands they write are read only after this.
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0) trace_stamp(args.trace, 2);
         const uint64_t pol = ptx::policy_evict_normal();
         int s = 0;
         uint32_t ph = 0;
@@ -436,6 +475,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int s = 0;
         uint32_t ph = 0, buf = 0, aph = 0;
         SchedReader<CG> sched;
+        bool traced_mma = false;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
             const uint32_t idesc = t < args.full_items ? idesc_full : idesc_half;
             int tm_, tn_, part_, kb0, kb1, ks_;
@@ -450,6 +490,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     ptx::tc_fence_after();
                 }
                 ptx::mbar_wait(&full[s], ph);
+                if (lane == 0 && kb == kb0 && !traced_mma) { trace_stamp(args.trace, 3); traced_mma = true; }
                 ptx::tc_fence_after();
                 {
                     // whole warp, converged: descriptors are warp-uniform; one
@@ -486,6 +527,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
+        if (lane == 0) trace_stamp(args.trace, 4);
     }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
@@ -498,6 +540,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         float *const *epi_gbase = args.gather_win != nullptr ? gbase : nullptr;
         uint32_t buf = 0, aph = 0;
         SchedReader<CG> sched;
+        bool traced_epi = false;
         for (int t = sched.next(sfull, sempty, stile, lane); t >= 0; t = sched.next(sfull, sempty, stile, lane)) {
             int tm, tn, part, kb0, kb1, ks;
             decode_item(t, args, tm, tn, part, kb0, kb1, ks);
@@ -509,6 +552,10 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint32_t tq = tq0 + half * cpw;
             const int64_t row0 = (int64_t)tm * Cfg::TILE_M + rank * ROWS_PER_CTA + 32 * q;
             const int64_t col0 = (int64_t)tn * BN + (part < 0 ? 0 : part * (BN / 2)) + half * cpw;
+            auto put = [&](int64_t col, const uint32_t(&v)[32]) {
+                if (args.tma_store) store_piece_tma(&tm_c, tbuf, lane, row0, col, args.ksplit > 1 ? ks : 0, v);
+                else store_piece(args, tbuf, lane, row0, col, v, epi_gbase, cbase);
+            };
             if (nchunks <= 0) {
                 // empty K range (never produced by the host's split-K plan): the
                 // partial contribution is zero; the MMA warp issues nothing for it
@@ -516,10 +563,11 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 32; i++) v[i] = 0u;
                 for (int qq = 0; qq < pieces; qq++)
-                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase, cbase);
+                    put(col0 + qq * 32, v);
             } else if (nchunks == 1) {
                 // whole K accumulated in TMEM: stream 32-column pieces to C
                 ptx::mbar_wait(&tfull[buf], aph);
+                if (e == 0 && lane == 0 && !traced_epi) { trace_stamp(args.trace, 5); traced_epi = true; }
                 ptx::tc_fence_after();
 #pragma unroll 1
                 for (int qq = 0; qq < pieces; qq++) {
@@ -531,7 +579,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     }
-                    store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase, cbase);
+                    put(col0 + qq * 32, v);
                 }
                 buf ^= 1;
                 if (buf == 0) aph ^= 1;
@@ -541,6 +589,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
                 for (int c = 0; c < nchunks; c++) {
                     ptx::mbar_wait(&tfull[buf], aph);
+                    if (e == 0 && lane == 0 && !traced_epi) { trace_stamp(args.trace, 5); traced_epi = true; }
                     ptx::tc_fence_after();
                     const uint32_t taddr = tq + buf * BN;
 #pragma unroll
@@ -570,7 +619,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         uint32_t v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
-                        store_piece(args, tbuf, lane, row0, col0 + qq * 32, v, epi_gbase, cbase);
+                        put(col0 + qq * 32, v);
                     }
                 }
             }
@@ -578,11 +627,14 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         // fused gather: make this thread's peer stores visible system-wide before
         // the kernel completes (the host orders a cross-rank barrier after it)
         if (epi_gbase != nullptr) __threadfence_system();
+        if (args.tma_store && lane == 0) ptx::bulk_wait_all();  // this warp's TMA stores complete
+        if (e == 0 && lane == 0) trace_stamp(args.trace, 6);
     }
 
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
+    if (threadIdx.x == 0) trace_stamp(args.trace, 7);
     if (warp == 2) ptx::tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
 }
 

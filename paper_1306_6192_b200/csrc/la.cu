@@ -101,6 +101,25 @@ static la_status make_tmap_f64(CUtensorMap *map, const double *ptr, int64_t rows
     return LA_OK;
 }
 
+// Output map for the GEMM's TMA-store epilogue: fp32 {cols, rows, slices}, row
+// stride ldc floats (ldc % 4 == 0), slice stride rows * ldc, 32 x 32 boxes,
+// 128-byte swizzle (the epilogue's smem layout).
+static la_status make_tmap_c(CUtensorMap *map, float *ptr, int64_t rows, int64_t cols, int64_t ldc, int64_t slices) {
+    auto enc = get_encoder();
+    if (!enc) return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)slices};
+    cuuint64_t strides[2] = {(cuuint64_t)ldc * sizeof(float), (cuuint64_t)(rows * ldc) * sizeof(float)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled (C) failed (%d) rows=%lld cols=%lld ldc=%lld", (int)r,
+                    (long long)rows, (long long)cols, (long long)ldc);
+    return LA_OK;
+}
+
 // ---- optional per-kernel device timing (bench.py roofline) ----------------
 struct TimedSpan {
     cudaEvent_t a, b;
@@ -389,10 +408,32 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
             args.num_items = (int32_t)(tiles + R);
         }
     }
+    // TMA-store epilogue for plain row-major outputs (C or the split-K partial
+    // slices); LA_TMA_STORE=0 selects the per-thread stores (A/B knob).
+    CUtensorMap tm_c;
+    memset(&tm_c, 0, sizeof tm_c);
+    {
+        float *base = args.ksplit > 1 ? args.partial : args.C;
+        const bool env_off = getenv("LA_TMA_STORE") && atoi(getenv("LA_TMA_STORE")) == 0;
+        args.tma_store = !env_off && out.cstride == 1 && out.half_rows == 0 && out.gather_win == nullptr &&
+                         ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0 && n < ((int64_t)1 << 31) &&
+                         pc < ((int64_t)1 << 31);
+        if (args.tma_store && (s = make_tmap_c(&tm_c, base, n, pc, ldc, args.ksplit)) != LA_OK) return s;
+    }
+    args.trace = nullptr;
 #ifdef LA_DIAGNOSTICS
     // Energy diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip
     // MMAs.  Compiled in only with LA_BUILD_DIAGNOSTICS=1 at build time.
     args.debug = getenv("LA_DEBUG_KERNEL") ? atoi(getenv("LA_DEBUG_KERNEL")) : 0;
+    // LA_DIAG_TRACE=1: per-CTA globaltimer stamps, printed after the launch
+    // (host-synchronising; diagnostics only)
+    static int64_t *trace_buf = nullptr;
+    const bool trace_on = getenv("LA_DIAG_TRACE") && atoi(getenv("LA_DIAG_TRACE")) != 0;
+    if (trace_on) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * sizeof(int64_t) * 1024);
+        cudaMemsetAsync(trace_buf, 0, 8 * sizeof(int64_t) * 1024, st);
+        args.trace = trace_buf;
+    }
 #else
     args.debug = 0;
 #endif
@@ -439,12 +480,35 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     la_attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = la_attr;
     lc.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&lc, kern, ta_hi, ta_lo, tb_hi, tb_lo, args);
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, ta_hi, ta_lo, tb_hi, tb_lo, tm_c, args);
     if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
     (*launches)++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gemm kernel launch", __FILE__, __LINE__);
     if (sync_buf) cudaFreeAsync(sync_buf, st);
+#ifdef LA_DIAGNOSTICS
+    if (args.trace) {
+        const int nb = clusters * CG;
+        std::vector<int64_t> h((size_t)nb * 8);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), args.trace, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost);
+        int64_t t0s = INT64_MAX;
+        for (int b = 0; b < nb; b++) if (h[b * 8]) t0s = std::min(t0s, h[b * 8]);
+        static const char *names[8] = {"entry", "setup done", "producer past griddepcontrol.wait",
+                                       "MMA: first stage full", "MMA: last commit", "epilogue: first chunk ready",
+                                       "epilogue: stores done", "exit sync done"};
+        fprintf(stderr, "la_diag_trace grid=%d n=%lld p=%lld num_kb=%d kc=%d ksplit=%d (us after first entry)\n", nb,
+                (long long)n, (long long)pc, args.num_kb, args.kc, args.ksplit);
+        for (int k = 0; k < 8; k++) {
+            std::vector<double> v;
+            for (int b = 0; b < nb; b++) if (h[b * 8 + k]) v.push_back((h[b * 8 + k] - t0s) * 1e-3);
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            fprintf(stderr, "la_diag_trace %-36s min %9.2f med %9.2f max %9.2f (%zu CTAs)\n", names[k], v.front(),
+                    v[v.size() / 2], v.back(), v.size());
+        }
+    }
+#endif
     la_status rs = timing_end(st, t0, TIMED_GEMM);
     if (rs != LA_OK) return rs;
     if (args.ksplit > 1) {

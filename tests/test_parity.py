@@ -370,3 +370,17 @@ def test_concurrent_host_threads(la):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("n,m,p", [(300, 500, 200), (1000, 2000, 1500), (257, 64, 260), (512, 16384, 512),
+                                   (4096, 256, 4096)])
+def test_tma_store_epilogue_equals_thread_stores(la, n, m, p, monkeypatch):
+    """The TMA-store epilogue (hardware clipping at ragged edges, split-K
+    partial slices through a 3-D map) writes exactly what the per-thread
+    stores write."""
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    tma = la.gemm(A, B)
+    monkeypatch.setenv("LA_TMA_STORE", "0")
+    thr = la.gemm(A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(tma, thr)
