@@ -57,3 +57,24 @@ def test_fuzz_cgemm_dgemm_integer_exact(la, n, m, p):
     Bd = inputs.generate_f64(m, p, 1, "integer")
     D = la.dgemm(Ad.cuda(), Bd.cuda()).cpu().numpy()
     assert np.array_equal(D, oracle.dgemm(Ad.numpy(), Bd.numpy()))
+
+
+# Degenerate aspect ratios: dot products, outer products, single rows/columns,
+# very long K (split-K with many pieces), K = 1.  Integer inputs: exact.
+EXTREME = [(1, 65536, 1), (1, 1, 4096), (4096, 1, 1), (2, 200000, 3), (4096, 1, 4096), (1, 70000, 1000),
+           (1000, 70000, 1), (7, 3, 9000), (9000, 3, 7), (33, 123457, 65)]
+
+
+@pytest.mark.parametrize("n,m,p", EXTREME)
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_extreme_shapes_integer_exact(la, n, m, p, mode):
+    """Integer inputs in [-8, 8]: the product is exact in both modes (TF32
+    represents these integers exactly, and every partial sum stays < 2^24)."""
+    A = inputs.generate(n, m, 0, "integer", seed=n + 3 * m + 7 * p)
+    B = inputs.generate(m, p, 1, "integer", seed=n + 3 * m + 7 * p)
+    la.set_mode(mode)
+    try:
+        C = la.gemm(A.cuda(), B.cuda()).cpu().numpy()
+    finally:
+        la.set_mode("3xtf32")
+    assert np.array_equal(C, oracle.gemm(A.numpy(), B.numpy(), threads=8))
