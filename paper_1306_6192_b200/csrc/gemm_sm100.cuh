@@ -185,6 +185,12 @@ struct GemmCfg {
     static constexpr int NOPS = PASSES == 3 ? 2 : 1;        // hi (+ lo) tiles per operand
     static constexpr int A_TILE = ROWS_PER_CTA * KB * 4;    // 16 KB at KB = 32
     static constexpr int B_TILE = B_ROWS * KB * 4;
+    // A stage of KB = 64 holds two 128-byte swizzle atoms (K 0-31, 32-63) per
+    // operand, each loaded by its own TMA box; KB <= 32 is one atom.
+    static constexpr int ATOM_K = KB < 32 ? KB : 32;
+    static constexpr int ATOMS = KB / ATOM_K;
+    static constexpr int A_ATOM = ROWS_PER_CTA * ATOM_K * 4;
+    static constexpr int B_ATOM = B_ROWS * ATOM_K * 4;
     static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);  // per CTA
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * 32 * 32 * 4; // per-warp transpose buffers
     static constexpr int BAR_BYTES = 512;  // mbarriers, TMEM address, tile ids; CLC response at +256
@@ -410,19 +416,18 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 } else if (lane == 0) {
                     const int32_t k0 = kb * KB;
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], CG * Cfg::STAGE_BYTES);
-                    if constexpr (CG == 1) {
-                        ptx::tma_load_2d(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
-                        ptx::tma_load_2d(b_tile(s, 0), &tm_b_hi, &full[s], k0, n0, pol);
+                    auto load = [&](uint8_t *dst, const CUtensorMap *map, int32_t kc0, int32_t row) {
+                        if constexpr (CG == 1) ptx::tma_load_2d(dst, map, &full[s], kc0, row, pol);
+                        else ptx::tma_load_2d_pair(dst, map, &full[s], kc0, row, pol);
+                    };
+#pragma unroll
+                    for (int at = 0; at < Cfg::ATOMS; at++) {
+                        const int32_t ka = k0 + at * Cfg::ATOM_K;
+                        load(a_tile(s, 0) + at * Cfg::A_ATOM, &tm_a_hi, ka, m0);
+                        load(b_tile(s, 0) + at * Cfg::B_ATOM, &tm_b_hi, ka, n0);
                         if constexpr (PASSES == 3) {
-                            ptx::tma_load_2d(a_tile(s, 1), &tm_a_lo, &full[s], k0, m0, pol);
-                            ptx::tma_load_2d(b_tile(s, 1), &tm_b_lo, &full[s], k0, n0, pol);
-                        }
-                    } else {
-                        ptx::tma_load_2d_pair(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
-                        ptx::tma_load_2d_pair(b_tile(s, 0), &tm_b_hi, &full[s], k0, n0, pol);
-                        if constexpr (PASSES == 3) {
-                            ptx::tma_load_2d_pair(a_tile(s, 1), &tm_a_lo, &full[s], k0, m0, pol);
-                            ptx::tma_load_2d_pair(b_tile(s, 1), &tm_b_lo, &full[s], k0, n0, pol);
+                            load(a_tile(s, 1) + at * Cfg::A_ATOM, &tm_a_lo, ka, m0);
+                            load(b_tile(s, 1) + at * Cfg::B_ATOM, &tm_b_lo, ka, n0);
                         }
                     }
                 }
@@ -502,12 +507,15 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t bl = ptx::smem_u32(b_tile(s, PASSES == 3 ? 1 : 0));
 #pragma unroll
                     for (int j = 0; j < KB / 8; j++) {  // K = 8 per tf32 MMA = 32 bytes of a swizzled row
-                        const uint64_t dah = ptx::sdesc_kmajor<KB>(ah + 32 * j);
-                        const uint64_t dbh = ptx::sdesc_kmajor<KB>(bh + 32 * j);
+                        constexpr int JA = Cfg::ATOM_K / 8;  // MMA K steps per swizzle atom
+                        const uint32_t oa = (j / JA) * Cfg::A_ATOM + 32 * (j % JA);
+                        const uint32_t ob = (j / JA) * Cfg::B_ATOM + 32 * (j % JA);
+                        const uint64_t dah = ptx::sdesc_kmajor<Cfg::ATOM_K>(ah + oa);
+                        const uint64_t dbh = ptx::sdesc_kmajor<Cfg::ATOM_K>(bh + ob);
                         const uint32_t acc = (chunk_first && j == 0) ? 0u : 1u;
                         if constexpr (PASSES == 3) {
-                            const uint64_t dal = ptx::sdesc_kmajor<KB>(al + 32 * j);
-                            const uint64_t dbl = ptx::sdesc_kmajor<KB>(bl + 32 * j);
+                            const uint64_t dal = ptx::sdesc_kmajor<Cfg::ATOM_K>(al + oa);
+                            const uint64_t dbl = ptx::sdesc_kmajor<Cfg::ATOM_K>(bl + ob);
                             ptx::mma_tf32_elect<CG>(d, dah, dbl, idesc, acc);  // hi . lo'
                             ptx::mma_tf32_elect<CG>(d, dal, dbh, idesc, 1u);   // lo . hi'
                             ptx::mma_tf32_elect<CG>(d, dah, dbh, idesc, 1u);   // hi . hi'

@@ -284,11 +284,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     la_status s;
     const float *bh = ops.b_hi + j0 * ops.mp, *bl = ops.b_lo + j0 * ops.mp;
-    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA, KB)) != LA_OK) return s;
-    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS, KB)) != LA_OK) return s;
+    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA, Cfg::ATOM_K)) != LA_OK) return s;
+    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS, Cfg::ATOM_K)) != LA_OK) return s;
     if (PASSES == 3) {
-        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, ROWS_PER_CTA, KB)) != LA_OK) return s;
-        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, Cfg::B_ROWS, KB)) != LA_OK) return s;
+        if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, ROWS_PER_CTA, Cfg::ATOM_K)) != LA_OK) return s;
+        if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, Cfg::B_ROWS, Cfg::ATOM_K)) != LA_OK) return s;
     } else {
         ta_lo = ta_hi;
         tb_lo = tb_hi;
@@ -570,6 +570,17 @@ la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands 
     if (ops.passes == 3) {
         if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
+    }
+    // plain TF32, long power-capped runs: K-blocks of 64 (two swizzle atoms per
+    // stage, 3 x 64 KB) halve the per-stage barrier and issue work of the single
+    // pass -- measured +2.6..4.7% at n = 16384, -0.7..1.6% at n = 4096 / 8192
+    // (more, smaller stages win when the clock is not capped), hence only from
+    // 2^41 multiply-adds up.  LA_TF32_KB=32|64 forces either (A/B knob).
+    const char *kbe = getenv("LA_TF32_KB");
+    const bool kb64 = kbe ? atoi(kbe) == 64 : (double)n * (double)pc * (double)m >= 2199023255552.0;
+    if (kb64) {
+        if (cg == 2) return launch_gemm<2, 256, 3, 1, 64>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
+        return launch_gemm<1, 128, 3, 1, 64>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
     }
     if (cg == 2) return launch_gemm<2, 256, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
     return launch_gemm<1, 128, kStages1, 1>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);

@@ -384,3 +384,21 @@ def test_tma_store_epilogue_equals_thread_stores(la, n, m, p, monkeypatch):
     thr = la.gemm(A, B)
     torch.cuda.synchronize()
     assert torch.equal(tma, thr)
+
+
+@pytest.mark.parametrize("n,m,p", [(300, 500, 200), (1000, 2000, 1500), (256, 4100, 384)])
+def test_tf32_kblock_64_equals_32(la, n, m, p, monkeypatch):
+    """Plain TF32 with 64-wide K-blocks (two swizzle atoms per stage) and with
+    32-wide ones: same MMAs in the same order, bitwise equal."""
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    la.set_mode("tf32")
+    try:
+        monkeypatch.setenv("LA_TF32_KB", "64")
+        c64 = la.gemm(A, B)
+        monkeypatch.setenv("LA_TF32_KB", "32")
+        c32 = la.gemm(A, B)
+        torch.cuda.synchronize()
+    finally:
+        la.set_mode("3xtf32")
+    assert torch.equal(c64, c32)
