@@ -86,7 +86,7 @@ def la1():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,m,p,panels", [(512, 384, 640, 1), (512, 384, 640, 3), (300, 1000, 1500, 4),
-                                          (4096, 2048, 4096, 4)])
+                                          (4096, 2048, 4096, 4), (300, 1000, 1501, 4), (257, 70, 999, 2)])
 def test_multi_one_rank_bitwise_equals_single(la1, n, m, p, panels, monkeypatch):
     la = la1
     la.set_option("panels", panels)
@@ -102,6 +102,25 @@ def test_multi_one_rank_bitwise_equals_single(la1, n, m, p, panels, monkeypatch)
     pc = -(-(-(-p // panels)) // 128) * 128            # panel width: ceil(p / panels) up to 128
     n_panels = -(-p // pc)
     assert la.last_launch_count() == 1 + 2 * n_panels   # split A, then split B + GEMM per panel
+
+
+@pytest.mark.gpu
+def test_multi_one_rank_tf32_mode(la1, monkeypatch):
+    """Plain TF32 mode through the multi path equals la_gemm in the same mode."""
+    la = la1
+    la.set_option("panels", 3)
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    n, m, p = 640, 512, 1000
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    la.set_mode("tf32")
+    try:
+        ref = la.gemm(A, B)
+        Cl = torch.empty(n, p, device="cuda")
+        la.gemm_multi(n, m, p, A, B, Cl, None, root=0, ngpu=1)
+        torch.cuda.synchronize()
+    finally:
+        la.set_mode("3xtf32")
+    assert torch.equal(Cl, ref)
 
 
 @pytest.mark.gpu
