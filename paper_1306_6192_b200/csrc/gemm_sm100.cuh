@@ -85,6 +85,7 @@ struct GemmArgs {
     int32_t *wave_sync; // static stride only, optional: arrival counters (zeroed per launch), one per
                         // (wave, K phase of sync_kb K-blocks)
     int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
+    int32_t wave_slots; // counters in wave_sync; wave_sync[wave_slots] is the give-up flag
     int32_t debug;      // diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip MMAs
     int64_t *trace;     // diagnostics only: per-CTA globaltimer stamps (8 per CTA), or nullptr
     // 1: plain row-major output (cstride 1, no half rows, no gather) stored by
@@ -145,8 +146,12 @@ static __global__ void __launch_bounds__(256) splitk_reduce_vec4_kernel(const fl
 // have arrived, so the clusters that share A rows / B columns stream through K
 // together and reuse each other's slabs in L2 instead of re-reading them from
 // HBM.
-__device__ __forceinline__ void wave_barrier(int32_t *ctr, int target) {
+__device__ __forceinline__ void wave_barrier(int32_t *ctr, int target, int32_t *give_up) {
     atomicAdd(ctr, 1);
+    // a wave that cannot be co-resident (other kernels hold SMs) would pay the
+    // full timeout at every phase: after the first timeout every producer of
+    // this launch stops waiting
+    if (*reinterpret_cast<volatile int32_t *>(give_up)) return;
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
@@ -155,7 +160,10 @@ __device__ __forceinline__ void wave_barrier(int32_t *ctr, int target) {
         if (v >= target) break;
         uint64_t t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 200000) break;
+        if (t1 - t0 > 200000) {
+            atomicExch(give_up, 1);
+            break;
+        }
         __nanosleep(128);
     }
 }
@@ -407,7 +415,9 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const int phases = (num_kb + args.sync_kb - 1) / args.sync_kb;
             for (int kb = kb0; kb < kb1; kb++) {
                 if (args.wave_sync != nullptr && kb % args.sync_kb == 0) {
-                    if (lane == 0) wave_barrier(args.wave_sync + wave * phases + kb / args.sync_kb, wave_target);
+                    if (lane == 0)
+                        wave_barrier(args.wave_sync + wave * phases + kb / args.sync_kb, wave_target,
+                                     args.wave_sync + args.wave_slots);
                     __syncwarp();
                 }
                 ptx::mbar_wait(&empty[s], ph ^ 1);

@@ -438,6 +438,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.debug = 0;
 #endif
     args.wave_sync = nullptr;
+    args.wave_slots = 0;
     args.sync_kb = args.num_kb;
     void *sync_buf = nullptr;
     // K-phase alignment of the static schedule (gemm_sm100.cuh wave_barrier):
@@ -459,9 +460,10 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
         const int64_t phases = (args.num_kb + args.sync_kb - 1) / args.sync_kb;
         const size_t nw = (size_t)((args.num_items + clusters - 1) / clusters * phases);
-        cudaError_t e = cudaMallocFromPoolAsync(&sync_buf, nw * sizeof(int32_t), g_state.pool, st);
+        args.wave_slots = (int32_t)nw;
+        cudaError_t e = cudaMallocFromPoolAsync(&sync_buf, (nw + 1) * sizeof(int32_t), g_state.pool, st);
         if (e != cudaSuccess) return cuda_fail(e, "wave sync buffer", __FILE__, __LINE__);
-        e = cudaMemsetAsync(sync_buf, 0, nw * sizeof(int32_t), st);
+        e = cudaMemsetAsync(sync_buf, 0, (nw + 1) * sizeof(int32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "wave sync memset", __FILE__, __LINE__);
         args.wave_sync = static_cast<int32_t *>(sync_buf);
     }
