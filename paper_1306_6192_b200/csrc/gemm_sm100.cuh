@@ -107,6 +107,7 @@ constexpr int MAX_GATHER_PEERS = 8;  // one NVLink / NVSwitch domain of 8 GPUs
 // (deterministic).  HBM-bound, 4 (ksplit + 1) bytes per element.
 static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ part, float *__restrict__ C,
                                                             int64_t count, int ksplit) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL): the GEMM's partials first
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x) {
         float acc = part[i];
@@ -126,6 +127,7 @@ __device__ __forceinline__ void trace_stamp(int64_t *trace, int k) {
 static __global__ void __launch_bounds__(256) splitk_reduce_vec4_kernel(const float4 *__restrict__ part,
                                                                  float4 *__restrict__ C, int64_t count4,
                                                                  int ksplit) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4;
          i += (int64_t)gridDim.x * blockDim.x) {
         float4 acc = __ldcs(part + i);
@@ -344,6 +346,9 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = threadIdx.x & 31;
     if (threadIdx.x == 0) trace_stamp(args.trace, 0);
+    // a dependent launched with programmatic serialization (the split-K
+    // reduction) may be scheduled now; it waits for this grid's completion
+    asm volatile("griddepcontrol.launch_dependents;");
     const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;  // CTA rank in the pair
     const int cluster_id = blockIdx.x / CG;
     const int num_clusters = gridDim.x / CG;

@@ -520,11 +520,24 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)g_state.sms * 8));
         cudaEvent_t t1;
         if ((rs = timing_begin(st, &t1)) != LA_OK) return rs;
+        // programmatic dependent launch: scheduled while the GEMM drains, the
+        // kernel's griddepcontrol.wait holds it until the partials are complete
+        cudaLaunchConfig_t rc = {};
+        rc.gridDim = dim3((unsigned)blocks);
+        rc.blockDim = dim3(256);
+        rc.stream = st;
+        cudaLaunchAttribute ra[1];
+        ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        ra[0].val.programmaticStreamSerializationAllowed = 1;
+        rc.attrs = ra;
+        rc.numAttrs = 1;
         if (vec)
-            splitk_reduce_vec4_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(args.partial),
-                                                              reinterpret_cast<float4 *>(args.C), work, args.ksplit);
+            e = cudaLaunchKernelEx(&rc, splitk_reduce_vec4_kernel, reinterpret_cast<const float4 *>(args.partial),
+                                   reinterpret_cast<float4 *>(args.C), work, args.ksplit);
         else
-            splitk_reduce_kernel<<<blocks, 256, 0, st>>>(args.partial, args.C, count, args.ksplit);
+            e = cudaLaunchKernelEx(&rc, splitk_reduce_kernel, static_cast<const float *>(args.partial), args.C,
+                                   count, args.ksplit);
+        if (e != cudaSuccess) return cuda_fail(e, "split-K reduce launch", __FILE__, __LINE__);
         (*launches)++;
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "split-K reduce launch", __FILE__, __LINE__);

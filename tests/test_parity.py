@@ -151,9 +151,13 @@ def test_fused_split_equals_separate_splits(la, n, m, p, monkeypatch):
     assert torch.equal(fused, sep)
 
 
-def test_graph_capture(la):
-    A, B = inputs.pair(512, 384, 640, "integer", device="cuda")
-    C = torch.empty(512, 640, device="cuda")
+@pytest.mark.parametrize("n,m,p", [(512, 384, 640), (512, 16384, 512), (1000, 2000, 1500)])
+def test_graph_capture(la, n, m, p):
+    """la_gemm inside a CUDA graph (stream-ordered workspace, programmatic
+    dependent launches of the GEMM and of the split-K reduction) replays to
+    the same result."""
+    A, B = inputs.pair(n, m, p, "integer", device="cuda")
+    C = torch.empty(n, p, device="cuda")
     la.gemm(A, B, out=C)
     torch.cuda.synchronize()
     ref = C.clone()
