@@ -129,6 +129,18 @@ LA_API la_status la_gemm(int64_t n, int64_t m, int64_t p, const float *d_A, cons
 LA_API la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B,
                        float *h_C, void *stream);
 
+/* `count` independent products of one shape from HOST buffers, returning after
+ * all of them completed: C_i = A_i . B_i for h_A[i], h_B[i], h_C[i] (arrays of
+ * `count` host pointers; each as in la_gemm_host).  Two device staging slots
+ * alternate, so the copy-in of product i + 1 overlaps the compute and copy-out
+ * of product i: with pinned buffers the PCIe copy engines stay busy across
+ * products (the serving-pipeline form of la_gemm_host).  Each product is
+ * bitwise equal to la_gemm_host on the same inputs.  The h_C[i] must not
+ * overlap each other or any input.  Errors: as la_gemm_host; INVALID_VALUE
+ * also for count < 1 or a NULL array. */
+LA_API la_status la_gemm_host_batch(int64_t count, int64_t n, int64_t m, int64_t p, const float *const *h_A,
+                                    const float *const *h_B, float *const *h_C, void *stream);
+
 /* Complex single-precision product (Table 2 "Complex Float" column, P:222-228;
  * complex multiply as in SPEC S:85-93):
  *   d_A : n x m complex64, row-major, interleaved (re, im) float pairs, device;

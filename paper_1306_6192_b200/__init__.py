@@ -29,7 +29,7 @@ OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3}
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
            "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times", "la_cgemm",
-           "la_add", "la_dgemm", "la_gather_alloc")
+           "la_add", "la_dgemm", "la_gather_alloc", "la_gemm_host_batch")
 
 
 class LaError(RuntimeError):
@@ -50,6 +50,7 @@ def _load() -> ctypes.CDLL:
         "la_get_option": ([ctypes.c_int, ctypes.POINTER(i64)], st),
         "la_gemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_gemm_host": ([i64, i64, i64, vp, vp, vp, vp], st),
+        "la_gemm_host_batch": ([i64, i64, i64, i64, vp, vp, vp, vp], st),
         "la_cgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_dgemm": ([i64, i64, i64, vp, vp, vp, vp], st),
         "la_gather_alloc": ([i64, ctypes.POINTER(ctypes.c_void_p)], st),
@@ -240,6 +241,39 @@ def gemm_host(A, B, out=None, stream=None):
         raise ValueError("out has the wrong shape")
     _check(_lib.la_gemm_host(n, m, p, pa, pb, pc, _stream_ptr(stream)), "la_gemm_host")
     return out
+
+
+def gemm_host_batch(As, Bs, outs=None, stream=None):
+    """la_gemm_host_batch: C_i = A_i . B_i for equal-shape lists of host float32
+    arrays (numpy or CPU tensors; pinned for overlap).  The copy-in of product
+    i + 1 overlaps the compute and copy-out of product i.  Returns the outputs."""
+    import torch
+    if len(As) != len(Bs) or len(As) == 0:
+        raise ValueError("As and Bs must be non-empty lists of equal length")
+    def arr(x):
+        if isinstance(x, torch.Tensor):
+            if x.device.type != "cpu" or x.dtype != torch.float32 or not x.is_contiguous():
+                raise TypeError("host tensors must be contiguous float32 on the CPU")
+            return x, x.data_ptr(), tuple(x.shape)
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        return x, x.ctypes.data, tuple(x.shape)
+    a = [arr(x) for x in As]
+    b = [arr(x) for x in Bs]
+    n, m = a[0][2]
+    m2, p = b[0][2]
+    if m != m2 or any(x[2] != (n, m) for x in a) or any(x[2] != (m, p) for x in b):
+        raise ValueError("all A must be n x m and all B m x p")
+    if outs is None:
+        outs = [np.empty((n, p), dtype=np.float32) for _ in As]
+    c = [arr(x) for x in outs]
+    if len(c) != len(a) or any(x[2] != (n, p) for x in c):
+        raise ValueError("outs must be len(As) arrays of shape (n, p)")
+    k = len(a)
+    pa = (ctypes.c_void_p * k)(*[x[1] for x in a])
+    pb = (ctypes.c_void_p * k)(*[x[1] for x in b])
+    pc = (ctypes.c_void_p * k)(*[x[1] for x in c])
+    _check(_lib.la_gemm_host_batch(k, n, m, p, pa, pb, pc, _stream_ptr(stream)), "la_gemm_host_batch")
+    return [x[0] for x in c]
 
 
 def shard_rows(n: int, rank: int, ngpu: int):

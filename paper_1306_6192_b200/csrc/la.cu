@@ -791,46 +791,24 @@ static int64_t host_panels() {
     return std::max<int64_t>(1, std::min<int64_t>(q, 64));
 }
 
-la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
-                       void *stream) {
-    std::lock_guard<std::recursive_mutex> lk(g_mutex);
-    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
-    if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
-    if (!h_A || !h_B || !h_C) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t ab = (size_t)(n * m) * 4, bb = (size_t)(m * p) * 4, cb = (size_t)(n * p) * 4;
-    const size_t need = ab + bb + cb + 3 * 256;
-    if (!g_state.h2d) {
-        LA_CK(cudaStreamCreateWithFlags(&g_state.h2d, cudaStreamNonBlocking));
-        LA_CK(cudaStreamCreateWithFlags(&g_state.d2h, cudaStreamNonBlocking));
-    }
-    if (g_state.staging_bytes < need) {
-        if (g_state.staging) {
-            LA_CK(cudaDeviceSynchronize());
-            LA_CK(cudaFree(g_state.staging));
-            g_state.staging = nullptr;
-            g_state.staging_bytes = 0;
-        }
-        cudaError_t e = cudaMalloc(&g_state.staging, need);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            return fail(LA_ERR_OUT_OF_MEMORY, "device staging of %zu bytes", need);
-        }
-        g_state.staging_bytes = need;
-    }
-    char *base = static_cast<char *>(g_state.staging);
-    float *dA = reinterpret_cast<float *>(base);
-    float *dB = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256);
-    float *dC = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256 + (bb + 255) / 256 * 256);
+}  // extern "C"
 
-    // 2-D transfer schedule: A in row panels, B in column panels (widths and
-    // heights multiples of the 256-wide tile), interleaved on the copy-in stream
-    // so that the fraction of A and of B on the device grow together.  Each
-    // panel that lands unlocks one rectangle of C -- its rows (or columns)
-    // against every panel of the other operand already present -- computed by
-    // one GEMM launch and copied out while later panels are still in flight.
-    // Every C element is produced by exactly one tile over the whole K range, in
-    // la_gemm's order.
+namespace la {
+
+// One product of a host call on device staging (dA, dB, dC): the 2-D transfer
+// schedule.  A travels in row panels and B in column panels (heights and widths
+// multiples of the 256-wide tile), interleaved on the copy-in stream so that
+// the fraction of A and of B on the device grow together.  Each panel that
+// lands unlocks one rectangle of C -- its rows (or columns) against every panel
+// of the other operand already present -- computed by one GEMM launch and
+// copied out while later panels are still in flight.  Every C element is
+// produced by exactly one tile over the whole K range, in la_gemm's order.
+// gate_h2d / gate_compute (optional): the staging slot's previous user has
+// finished computing from it / copying C out of it.
+static la_status host_item(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
+                           float *dA, float *dB, float *dC, const Operands &ops, cudaStream_t st,
+                           cudaEvent_t gate_h2d, cudaEvent_t gate_compute, cudaEvent_t done_compute,
+                           cudaEvent_t done_d2h, int *launches, HostTrace &tr) {
     const int64_t q = host_panels();
     auto panel = [q](int64_t len) {
         return len >= 2048 ? std::min(len, ((len + q - 1) / q + 255) / 256 * 256) : len;
@@ -838,37 +816,21 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     const int64_t rh = panel(n), pw = panel(p);
     const int64_t Qr = (n + rh - 1) / rh, Qc = (p + pw - 1) / pw;
     const int64_t tail_split = host_tail_split();
-    while ((int64_t)g_state.host_events.size() < 1 + 2 * (Qr + Qc) + 2 * tail_split) {
+    while ((int64_t)g_state.host_events.size() < 2 * (Qr + Qc) + 2 * tail_split) {
         cudaEvent_t e;
         LA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         g_state.host_events.push_back(e);
     }
-    cudaEvent_t ev_start = g_state.host_events[0];
-    cudaEvent_t *ev_a = &g_state.host_events[1], *ev_b = ev_a + Qr, *ev_c = ev_b + Qc;
+    // (events are re-recorded by later items only after every wait on them
+    // has been enqueued, so one set serves all items of a call)
+    cudaEvent_t *ev_a = &g_state.host_events[0], *ev_b = ev_a + Qr, *ev_c = ev_b + Qc;
     // arrival order: the operand whose present fraction is smaller goes next (A first)
     std::vector<std::pair<bool, int64_t>> order;  // (is_A, panel index)
     for (int64_t a = 0, bq = 0; a < Qr || bq < Qc;) {
         if (bq >= Qc || (a < Qr && a * Qc <= bq * Qr)) order.push_back({true, a++});
         else order.push_back({false, bq++});
     }
-
-    const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
-    void *ws = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync(&ws, operands_bytes(n, m, p, passes), g_state.pool, st);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LA_ERR_OUT_OF_MEMORY, "workspace");
-    }
-    const Operands ops = operands_carve(ws, n, m, p, passes);
-    int launches = 0;
-
-    HostTrace tr;
-    tr.on = getenv("LA_HOST_TRACE") && atoi(getenv("LA_HOST_TRACE")) != 0;
-    // the copy streams start after everything already queued on `st`
-    LA_CK(cudaEventRecord(ev_start, st));
-    LA_CK(cudaStreamWaitEvent(g_state.h2d, ev_start, 0));
-    LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_start, 0));
-    tr.mark("start", g_state.h2d);
+    if (gate_h2d) LA_CK(cudaStreamWaitEvent(g_state.h2d, gate_h2d, 0));
     for (const auto &o : order) {
         if (o.first) {
             const int64_t r0 = o.second * rh, rows = std::min(rh, n - r0);
@@ -884,6 +846,7 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
             tr.mark("h2d B" + std::to_string(o.second), g_state.h2d);
         }
     }
+    if (gate_compute) LA_CK(cudaStreamWaitEvent(st, gate_compute, 0));
     la_status s = LA_OK;
     int64_t rows_in = 0, cols_in = 0, regions = 0;
     for (const auto &o : order) {
@@ -895,7 +858,7 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
             Operands pan = ops;
             pan.a_hi = ops.a_hi + r0 * ops.mp;
             pan.a_lo = ops.a_lo + r0 * ops.mp;
-            s = split_a(r1 - r0, m, dA + r0 * m, pan, st, &launches);
+            s = split_a(r1 - r0, m, dA + r0 * m, pan, st, launches);
             rows_in = r1;
             c0 = 0;
             c1 = cols_in;
@@ -903,12 +866,12 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
             c0 = o.second * pw;
             c1 = std::min(p, c0 + pw);
             LA_CK(cudaStreamWaitEvent(st, ev_b[o.second], 0));
-            s = split_b(m, c0, c1 - c0, dB + c0, p, ops, st, &launches);
+            s = split_b(m, c0, c1 - c0, dB + c0, p, ops, st, launches);
             cols_in = c1;
             r0 = 0;
             r1 = rows_in;
         }
-        if (s != LA_OK) break;
+        if (s != LA_OK) return s;
         tr.mark(std::string("split ") + (o.first ? "A" : "B") + std::to_string(o.second), st);
         if (r1 <= r0 || c1 <= c0) continue;
         // the last two rectangles are computed in pieces along their long side
@@ -917,15 +880,15 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
         const bool by_rows = r1 - r0 >= c1 - c0;
         const int64_t len = by_rows ? r1 - r0 : c1 - c0;
         const int64_t step = std::max<int64_t>(256, ((len + pieces - 1) / pieces + 255) / 256 * 256);
-        for (int64_t x0 = 0; x0 < len && s == LA_OK; x0 += step) {
+        for (int64_t x0 = 0; x0 < len; x0 += step) {
             const int64_t x1 = std::min(len, x0 + step);
             const int64_t q0 = by_rows ? r0 + x0 : r0, q1 = by_rows ? r0 + x1 : r1;
             const int64_t k0 = by_rows ? c0 : c0 + x0, k1 = by_rows ? c1 : c0 + x1;
             Operands pan = ops;
             pan.a_hi = ops.a_hi + q0 * ops.mp;
             pan.a_lo = ops.a_lo + q0 * ops.mp;
-            s = gemm_run(q1 - q0, m, k0, k1 - k0, pan, dC + q0 * p, p, (int)g_state.max_sms, st, &launches);
-            if (s != LA_OK) break;
+            s = gemm_run(q1 - q0, m, k0, k1 - k0, pan, dC + q0 * p, p, (int)g_state.max_sms, st, launches);
+            if (s != LA_OK) return s;
             tr.mark("gemm " + std::to_string(q1 - q0) + "x" + std::to_string(k1 - k0), st);
             LA_CK(cudaEventRecord(ev_c[regions], st));
             LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_c[regions], 0));
@@ -935,6 +898,82 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
             tr.mark("d2h " + std::to_string(regions), g_state.d2h);
             regions++;
         }
+    }
+    LA_CK(cudaEventRecord(done_compute, st));
+    LA_CK(cudaEventRecord(done_d2h, g_state.d2h));
+    return LA_OK;
+}
+
+// `count` independent host products of one shape.  With count > 1 two device
+// staging slots alternate, so the copy-in of product i + 1 runs while product i
+// still computes and copies out (the copy engines stay busy across products).
+static la_status host_run(int64_t count, int64_t n, int64_t m, int64_t p, const float *const *hA,
+                          const float *const *hB, float *const *hC, cudaStream_t st) {
+    if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
+    if (count < 1) return fail(LA_ERR_INVALID_VALUE, "count must be >= 1");
+    if (n <= 0 || m <= 0 || p <= 0) return fail(LA_ERR_INVALID_VALUE, "dimensions must be >= 1");
+    if (n > (int64_t)1 << 31 || m > (int64_t)1 << 31 || p > (int64_t)1 << 31)
+        return fail(LA_ERR_UNSUPPORTED, "dimension exceeds 2^31 (TMA coordinates are int32)");
+    for (int64_t i = 0; i < count; i++)
+        if (!hA[i] || !hB[i] || !hC[i]) return fail(LA_ERR_INVALID_VALUE, "NULL matrix pointer (product %lld)",
+                                                    (long long)i);
+    const size_t ab = (size_t)(n * m) * 4, bb = (size_t)(m * p) * 4, cb = (size_t)(n * p) * 4;
+    const size_t slot_bytes = (ab + 255) / 256 * 256 + (bb + 255) / 256 * 256 + (cb + 255) / 256 * 256;
+    const int slots = count > 1 ? 2 : 1;
+    const size_t need = slots * slot_bytes;
+    if (!g_state.h2d) {
+        LA_CK(cudaStreamCreateWithFlags(&g_state.h2d, cudaStreamNonBlocking));
+        LA_CK(cudaStreamCreateWithFlags(&g_state.d2h, cudaStreamNonBlocking));
+    }
+    while (g_state.slot_events.size() < 5) {
+        cudaEvent_t e;
+        LA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        g_state.slot_events.push_back(e);
+    }
+    if (g_state.staging_bytes < need) {
+        if (g_state.staging) {
+            LA_CK(cudaDeviceSynchronize());
+            LA_CK(cudaFree(g_state.staging));
+            g_state.staging = nullptr;
+            g_state.staging_bytes = 0;
+        }
+        cudaError_t e = cudaMalloc(&g_state.staging, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(LA_ERR_OUT_OF_MEMORY, "device staging of %zu bytes", need);
+        }
+        g_state.staging_bytes = need;
+    }
+    const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&ws, operands_bytes(n, m, p, passes), g_state.pool, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LA_ERR_OUT_OF_MEMORY, "workspace");
+    }
+    // one operand workspace serves every product: their splits and GEMMs are
+    // ordered on `st`
+    const Operands ops = operands_carve(ws, n, m, p, passes);
+    int launches = 0;
+    HostTrace tr;
+    tr.on = getenv("LA_HOST_TRACE") && atoi(getenv("LA_HOST_TRACE")) != 0;
+    cudaEvent_t ev_start = g_state.slot_events[0];
+    cudaEvent_t *done_compute = &g_state.slot_events[1], *done_d2h = &g_state.slot_events[3];
+    // the copy streams start after everything already queued on `st`
+    LA_CK(cudaEventRecord(ev_start, st));
+    LA_CK(cudaStreamWaitEvent(g_state.h2d, ev_start, 0));
+    LA_CK(cudaStreamWaitEvent(g_state.d2h, ev_start, 0));
+    tr.mark("start", g_state.h2d);
+    la_status s = LA_OK;
+    for (int64_t i = 0; i < count && s == LA_OK; i++) {
+        const int sl = (int)(i % slots);
+        char *base = static_cast<char *>(g_state.staging) + sl * slot_bytes;
+        float *dA = reinterpret_cast<float *>(base);
+        float *dB = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256);
+        float *dC = reinterpret_cast<float *>(base + (ab + 255) / 256 * 256 + (bb + 255) / 256 * 256);
+        const bool reuse = i >= slots;
+        s = host_item(n, m, p, hA[i], hB[i], hC[i], dA, dB, dC, ops, st, reuse ? done_compute[sl] : nullptr,
+                      reuse ? done_d2h[sl] : nullptr, done_compute[sl], done_d2h[sl], &launches, tr);
     }
     cudaFreeAsync(ws, st);
     g_state.last_launches = launches;
@@ -947,6 +986,23 @@ la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const 
     LA_CK(cudaStreamSynchronize(st));
     tr.dump();
     return LA_OK;
+}
+
+}  // namespace la
+
+extern "C" {
+
+la_status la_gemm_host(int64_t n, int64_t m, int64_t p, const float *h_A, const float *h_B, float *h_C,
+                       void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
+    return host_run(1, n, m, p, &h_A, &h_B, &h_C, static_cast<cudaStream_t>(stream));
+}
+
+la_status la_gemm_host_batch(int64_t count, int64_t n, int64_t m, int64_t p, const float *const *h_A,
+                             const float *const *h_B, float *const *h_C, void *stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
+    if (!h_A || !h_B || !h_C) return fail(LA_ERR_INVALID_VALUE, "NULL pointer array");
+    return host_run(count, n, m, p, h_A, h_B, h_C, static_cast<cudaStream_t>(stream));
 }
 
 // Complex single-precision product (Table 2 "Complex Float") through
@@ -1127,6 +1183,8 @@ la_status la_finalize(void) {
     g_state.staging = nullptr;
     for (auto e : g_state.host_events) cudaEventDestroy(e);
     g_state.host_events.clear();
+    for (auto e : g_state.slot_events) cudaEventDestroy(e);
+    g_state.slot_events.clear();
     if (g_state.h2d) cudaStreamDestroy(g_state.h2d);
     if (g_state.d2h) cudaStreamDestroy(g_state.d2h);
     g_state.h2d = g_state.d2h = nullptr;

@@ -29,6 +29,7 @@ struct State {
     bool kernel_timing = false;
     cudaStream_t h2d = nullptr, d2h = nullptr;  // la_gemm_host copy streams
     std::vector<cudaEvent_t> host_events;
+    std::vector<cudaEvent_t> slot_events;  // la_gemm_host(_batch): start + per-slot completion
 };
 
 // Event pairs bracketing split and GEMM launches (LA_OPT_KERNEL_TIMING).

@@ -406,3 +406,33 @@ def test_tf32_kblock_64_equals_32(la, n, m, p, monkeypatch):
     finally:
         la.set_mode("3xtf32")
     assert torch.equal(c64, c32)
+
+
+@pytest.mark.parametrize("n,m,p,count", [(300, 500, 200, 3), (2300, 700, 2900, 3), (4096, 1024, 2048, 4)])
+def test_host_batch_products_equal_single_calls(la, n, m, p, count, monkeypatch):
+    """la_gemm_host_batch: distinct products through two alternating staging
+    slots (copy-in of i + 1 overlapping product i), each bitwise equal to
+    la_gemm on the same inputs."""
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    As, Bs, refs = [], [], []
+    for i in range(count):
+        A = inputs.generate(n, m, 0, "stress", seed=1000 + i, device="cuda")
+        B = inputs.generate(m, p, 1, "stress", seed=2000 + i, device="cuda")
+        refs.append(la.gemm(A, B).cpu())
+        As.append(A.cpu().pin_memory())
+        Bs.append(B.cpu().pin_memory())
+    outs = [torch.empty(n, p).pin_memory() for _ in range(count)]
+    la.gemm_host_batch(As, Bs, outs)
+    for C, R in zip(outs, refs):
+        assert torch.equal(C, R)
+
+
+def test_host_batch_errors(la):
+    A = np.zeros((4, 4), dtype=np.float32)
+    lib = la._lib
+    import ctypes
+    arr = (ctypes.c_void_p * 1)(A.ctypes.data)
+    assert lib.la_gemm_host_batch(0, 4, 4, 4, arr, arr, arr, None) == la.LA_ERR_INVALID_VALUE
+    assert lib.la_gemm_host_batch(1, 4, 4, 4, None, arr, arr, None) == la.LA_ERR_INVALID_VALUE
+    nul = (ctypes.c_void_p * 1)(None)
+    assert lib.la_gemm_host_batch(1, 4, 4, 4, arr, nul, arr, None) == la.LA_ERR_INVALID_VALUE
