@@ -44,6 +44,23 @@ int main(void) {
                 break;
             }
         }
+    /* two products through the pipelined batch entry point: C2 = A . B2, C3 = A . B */
+    float *B2 = malloc(sizeof(float) * m * p), *C2 = malloc(sizeof(float) * n * p), *C3 = malloc(sizeof(float) * n * p);
+    if (!B2 || !C2 || !C3) return 1;
+    for (int64_t i = 0; i < m * p; i++) B2[i] = -B[i];
+    {
+        const float *as[2] = {A, A}, *bs[2] = {B2, B};
+        float *cs[2] = {C2, C3};
+        bad |= check(la_gemm_host_batch(2, n, m, p, as, bs, cs, NULL), LA_OK, "la_gemm_host_batch");
+    }
+    for (int64_t i = 0; i < n * p && !bad; i++)
+        if (C2[i] != -C[i] || C3[i] != C[i]) {
+            fprintf(stderr, "batch product mismatch at %lld\n", (long long)i);
+            bad = 1;
+        }
+    free(B2);
+    free(C2);
+    free(C3);
     bad |= check(la_gemm_host(0, m, p, A, B, C, NULL), LA_ERR_INVALID_VALUE, "zero dimension");
     bad |= check(la_gemm_host(n, m, p, NULL, B, C, NULL), LA_ERR_INVALID_VALUE, "NULL A");
     bad |= check(la_set_mode((la_mode)7), LA_ERR_INVALID_VALUE, "bad mode");
@@ -51,6 +68,6 @@ int main(void) {
     free(A);
     free(B);
     free(C);
-    if (!bad) printf("abi_host: %lldx%lldx%lld exact, error paths ok\n", (long long)n, (long long)m, (long long)p);
+    if (!bad) printf("abi_host: %lldx%lldx%lld exact (single and batch), error paths ok\n", (long long)n, (long long)m, (long long)p);
     return bad;
 }
