@@ -1,0 +1,41 @@
+"""bench.py's JSON-line contract, checked without a GPU: the reference arm
+runs here (the oracle on the host cores), and the committed GPU line
+(profiles/bench_r01g.json) carries every key the driver reads."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config"}
+
+
+def test_reference_arm_line():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                        "--cpu-seconds", "1", "--n", "2048"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert BASE_KEYS <= set(line)
+    assert line["impl"] == "reference"
+    assert line["value"] > 0 and line["unit"] == "TFLOP/s" and line["higher_is_better"] is True
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+
+
+def test_committed_gpu_line_has_every_key():
+    line = json.load(open(os.path.join(ROOT, "profiles", "bench_r01g.json")))
+    assert BASE_KEYS <= set(line)
+    assert line["n_gpus"] == 1 and line["warmup"] >= 3
+    assert line["config"]["workload"] and "l2" in line["config"]
+    rf = line["roofline"]
+    assert rf["bound"] == "tensor" and rf["unit"] == "TFLOP/s"
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9 and rf["traffic"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    e2e = line["e2e"]
+    assert e2e["h2d_bytes_per_step"] == 2 * 4 * 16384 ** 2 and e2e["d2h_bytes_per_step"] == 4 * 16384 ** 2
+    assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert line["gpu_launches"] > 0
