@@ -46,7 +46,7 @@ def main():
     err = float((np.abs(got - ref) / S).max() / 2.0 ** -20)
     med = statistics.median(ts)
     tf = 2.0 * n ** 3 / (med * 1e-3) / 1e12
-    print(f"| C5 n=65536 (1 GPU) | 3xtf32 | {med:.1f} | {min(ts):.1f} | {tf:.1f} | {100 * 3 * tf / 1125.0:.1f} | "
+    print(f"| C5 n=65536 (1 GPU) | 3xtf32 | {med:.1f} | {min(ts):.1f} | - | {tf:.1f} | {100 * 3 * tf / 1125.0:.1f} | "
           f"{err:.3f} | (integer: tests/test_parity.py::test_n65536_indexing_sampled) | "
           f"oracle on {len(rows)}x{len(cols)} sampled elements |", flush=True)
 

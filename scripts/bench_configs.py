@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Fill the BASELINE.md rows: every BASELINE.json config that fits one GPU,
-3xTF32 (and TF32 where the config asks), timed with CUDA events, checked
+3xTF32 (and TF32 where the config asks), timed with CUDA events (and, up to
+n = 2048, as a CUDA graph of 20 calls so the host is out of the loop; TFLOP/s
+then come from the graph time), checked
 against the oracle, with the oracle's own host time beside it.
 
     python scripts/bench_configs.py > profiles/configs_r01.md
@@ -44,10 +46,34 @@ def time_gemm(A, B, C, reps):
     return statistics.median(ts), min(ts)
 
 
+def time_graph(A, B, C, calls=20, reps=5):
+    """Device time per call with the host out of the loop: `calls` la_gemm
+    captured in one CUDA graph, replayed `reps` times (median)."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        la.gemm(A, B, out=C, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(calls):
+            la.gemm(A, B, out=C, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / calls)
+    return statistics.median(ts)
+
+
 def main():
     la.init(0)
-    print("| config | mode | median ms | min ms | logical TFLOP/s | % TF32 datasheet (issued) | max err / (2^-20 S) | integer exact | oracle (host) |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("| config | mode | median ms (events per call) | min ms | graph ms/call | logical TFLOP/s | % TF32 datasheet (issued) | max err / (2^-20 S) | integer exact | oracle (host) |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
     for label, n, m, p, modes, full in CONFIGS:
         A, B = inputs.pair(n, m, p, "stress", device="cuda")
         C = torch.empty(n, p, device="cuda")
@@ -75,11 +101,13 @@ def main():
             la.set_mode(mode)
             reps = 50 if n <= 2048 else (20 if n <= 4096 else 5)
             med, mn = time_gemm(A, B, C, reps)
+            gms = time_graph(A, B, C) if n <= 2048 else None  # latency-bound sizes: host overhead out
             got = C[rows][:, cols].cpu().numpy().astype(np.float64)
             err = float((np.abs(got - ref) / S).max() / 2.0 ** -20)
             passes = 3 if mode == "3xtf32" else 1
-            tf = 2.0 * n * m * p / (med * 1e-3) / 1e12
-            print(f"| {label} | {mode} | {med:.3f} | {mn:.3f} | {tf:.1f} | {100 * passes * tf / TF32_PEAK:.1f} | "
+            tf = 2.0 * n * m * p / ((gms if gms else med) * 1e-3) / 1e12
+            gcol = f"{gms:.4f}" if gms else "-"
+            print(f"| {label} | {mode} | {med:.3f} | {mn:.3f} | {gcol} | {tf:.1f} | {100 * passes * tf / TF32_PEAK:.1f} | "
                   f"{err:.3f} | {int_ok if mode == '3xtf32' else '-'} | {oracle_note} |", flush=True)
         la.set_mode("3xtf32")
 
