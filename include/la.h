@@ -74,9 +74,10 @@ typedef enum {
 typedef enum {
     /* 3xTF32 only: K elements accumulated in tensor memory before the partial
      * sum is added into an fp32 register running sum (round-to-nearest).  0 =
-     * never (the whole K range accumulates in TMEM).  Rounded up to a multiple
-     * of 32.  Default 256: the tcgen05 tf32 accumulator truncates, and whole-K
-     * accumulation breaks the 2^-20 bound. */
+     * never (the whole K range accumulates in TMEM); > 0: that many, rounded up
+     * to a multiple of 32.  Default -1 (automatic): 64 for K <= 256, 128 for
+     * K <= 1024, 256 beyond -- the tcgen05 tf32 accumulator truncates at every
+     * MMA, and one long chunk breaks the 2^-20 bound. */
     LA_OPT_PROMOTE_K = 0,
     /* Upper bound on the number of SMs the GEMM kernel occupies (0 = all).  The
      * multi-GPU path uses it to leave SMs for NCCL. */

@@ -309,7 +309,17 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.num_kb = (int32_t)((m + KB - 1) / KB);
     // Promotion only in 3xTF32: plain TF32's 2^-9 bound is 2^11 times looser than
     // the truncation bias of whole-K accumulation (~3 x 2^-20 S at K = 16384).
-    const int64_t pk = PASSES == 3 ? g_state.promote_k : 0;
+    // Automatic interval (promote_k < 0, the default): the TMEM accumulator
+    // truncates at every MMA, so one chunk of K_c elements carries 3 K_c / 8
+    // truncations at the chunk's own magnitude; long K averages them out over
+    // many chunks (RN running sum), short K does not.  Measured worst case on
+    // random-sign inputs vs the exact product (scripts/positive_check.py):
+    // K = 256 in one chunk 0.79 x 2^-20 S, in chunks of 64 0.19; so chunks of
+    // 64 up to K = 256, 128 up to K = 1024, 256 beyond (where a finer interval
+    // costs 9-24% of throughput and buys nothing on these inputs).
+    int64_t pk = PASSES == 3 ? g_state.promote_k : 0;
+    const int64_t km = out.policy_k > 0 ? out.policy_k : m;
+    if (pk < 0) pk = km <= 256 ? 64 : (km <= 1024 ? 128 : 256);
     args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + KB - 1) / KB);
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
@@ -703,7 +713,7 @@ la_status la_set_option(la_option option, int64_t value) {
     std::lock_guard<std::recursive_mutex> lk(g_mutex);
     switch (option) {
         case LA_OPT_PROMOTE_K:
-            if (value < 0) return fail(LA_ERR_INVALID_VALUE, "promote_k must be >= 0");
+            if (value < -1) return fail(LA_ERR_INVALID_VALUE, "promote_k must be >= -1 (-1: automatic)");
             g_state.promote_k = value;
             return LA_OK;
         case LA_OPT_MAX_SMS:
@@ -1061,6 +1071,7 @@ la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const floa
     out.cstride = 2;
     out.half_rows = n;
     out.half_off = 1;
+    out.policy_k = m;
     s = gemm_run(n2, m2, 0, p, ops, d_C, 2 * p, (int)g_state.max_sms, st, &launches, out);
     e = cudaFreeAsync(ws, st);
     g_state.last_launches = launches;

@@ -20,7 +20,7 @@ struct State {
     // Accumulator promotion interval in K elements (0 = whole K in TMEM).
     // Default 256: the tcgen05 kind::tf32 accumulator truncates (probe in
     // tests/test_probe.py); promotion every 256 keeps 3xTF32 at ~0.06 x 2^-20 S.
-    int64_t promote_k = 256;
+    int64_t promote_k = -1;  // -1: automatic by K (launch_gemm)
     int64_t max_sms = 0;
     int64_t panels = 4;
     int last_launches = 0;
@@ -75,6 +75,11 @@ struct OutSpec {
     // multi-GPU path never does, so its result stays bitwise equal to la_gemm
     // without split-K)
     bool splitk_ok = false;
+    // K length the automatic promotion interval is chosen for (0: the GEMM's
+    // own K).  la_cgemm passes m for its 2m-long embedding, so zero-imaginary
+    // products stay bitwise equal to la_gemm (zero products do not change a
+    // truncating or a rounding sum).
+    int64_t policy_k = 0;
 };
 
 // C[:, j0:j0+pc] (n x pc block of a row-major matrix with row stride ldc) =

@@ -73,8 +73,10 @@ def test_options_roundtrip():
     la.set_option("panels", 6)
     assert la.get_option("panels") == 6
     la.set_option("panels", old)
+    la.set_option("promote_k", -1)              # automatic by K (the default)
+    assert la.get_option("promote_k") == -1
     with pytest.raises(la.LaError):
-        la.set_option("promote_k", -1)
+        la.set_option("promote_k", -2)
 
 
 def test_shard_rows_partition():

@@ -85,10 +85,12 @@ def test_cgemm_4096_sampled(la):
     _ccheck(A[rows].cpu(), B[:, cols].cpu(), C[rows][:, cols].cpu().numpy(), "random")
 
 
-def test_cgemm_real_inputs_match_la_gemm_bitwise(la):
+def test_cgemm_real_inputs_match_la_gemm_bitwise(la, monkeypatch):
     """Zero imaginary parts: the real part is the real product computed with the
-    same K-block order (the embedding appends m zero columns), so it equals
-    la_gemm bitwise and the imaginary part is exactly zero."""
+    same K-block order and promotion chunks (the embedding appends m zero
+    columns), so it equals la_gemm without split-K bitwise and the imaginary
+    part is exactly zero."""
+    monkeypatch.setenv("LA_SPLIT_K", "0")
     A = inputs.generate(300, 500, 0, "stress", device="cuda")
     B = inputs.generate(500, 200, 1, "stress", device="cuda")
     C = la.cgemm(A.to(torch.complex64), B.to(torch.complex64))
