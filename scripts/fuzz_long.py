@@ -36,6 +36,28 @@ while time.time() < t_end:
     seed = int(rng.integers(1, 2 ** 31))
     kind = rng.choice(["stress", "random", "integer"])
     mode = "tf32" if rng.random() < 0.25 else "3xtf32"
+    if rng.random() < 0.2:  # complex product (per-component bound with the complex scales)
+        n, m, p = max(1, n // 2), max(1, m // 2), max(1, p // 2)
+        A = torch.view_as_complex(inputs.generate(n, 2 * m, 0, kind, seed=seed).view(n, m, 2)).contiguous()
+        B = torch.view_as_complex(inputs.generate(m, 2 * p, 1, kind, seed=seed).view(m, p, 2)).contiguous()
+        la.set_mode(mode)
+        C = la.cgemm(A.cuda(), B.cuda()).cpu().numpy()
+        la.set_mode("3xtf32")
+        ref = oracle.cgemm(A.numpy(), B.numpy())
+        cases += 1
+        if kind == "integer":
+            ok = np.array_equal(C, ref)
+        else:
+            Sr, Si = oracle.cabs_scale(A.numpy(), B.numpy())
+            err = max(float((np.abs(C.real.astype(np.float64) - ref.real) / np.maximum(Sr, 1e-300)).max()),
+                      float((np.abs(C.imag.astype(np.float64) - ref.imag) / np.maximum(Si, 1e-300)).max()))
+            bound = 2.0 ** -20 if mode == "3xtf32" else 2.0 ** -9
+            ok = err <= bound
+            worst[mode] = max(worst[mode], err / bound)
+        if not ok:
+            fails += 1
+            print(f"FAIL complex n={n} m={m} p={p} kind={kind} mode={mode} seed={seed}", flush=True)
+        continue
     A = inputs.generate(n, m, 0, kind, seed=seed)
     B = inputs.generate(m, p, 1, kind, seed=seed)
     la.set_mode(mode)
