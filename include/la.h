@@ -36,7 +36,10 @@
  *  - LA_MODE_3XTF32 (default): a = hi + lo with hi = tf32 round-to-nearest
  *    (ties away) of a and lo = a - hi; c = sum(hi*hi' + hi*lo' + lo*hi') on
  *    the tcgen05 tensor pipe with fp32 accumulation.  Contract:
- *    |c - c_ref| <= 2^-20 * sum_r |a_ir||b_rj| per element, and value-exact
+ *    |c - c_ref| <= 2^-20 * sum_r |a_ir||b_rj| per element (c_ref = the fp32
+ *    Listing 1 loop; for same-sign inputs, where that loop's own error grows
+ *    toward gamma_m * sum|a||b|, c is at least as close to the exact product
+ *    as c_ref, within 2^-20 * sum -- DESIGN.md reading C14'), and value-exact
  *    (==) on integer-valued inputs whose partial sums stay below 2^24.
  *  - LA_MODE_TF32: one pass on hi only; contract 2^-9 * sum_r |a_ir||b_rj|.
  *  - Inputs must be finite; non-finite inputs are out of contract.
@@ -108,8 +111,9 @@ LA_API la_status la_get_option(la_option option, int64_t *value);
  *   n, m, p   : dimensions, each >= 1;
  *   d_A       : n x m row-major fp32, device;  d_B : m x p row-major fp32, device;
  *   d_C       : n x p row-major fp32, device, written exactly once per element.
- * Work: one split pass over A and over B into a library workspace, then one
- * persistent tcgen05 GEMM kernel; problems with few output tiles and a long K
+ * Work: one split pass over A and B into a library workspace (one launch when
+ * both take the vectorised kernels), then one persistent tcgen05 GEMM kernel
+ * (programmatic dependent launch); problems with few output tiles and a long K
  * split K across clusters and add one in-order reduction kernel (deterministic,
  * integer inputs still exact).  Errors: NOT_INITIALIZED, INVALID_VALUE
  * (dims, NULL, C overlapping A or B), OUT_OF_MEMORY, CUDA. */
@@ -194,8 +198,9 @@ LA_API la_status la_comm_init(const void *uid128, int rank, int ngpu);
  *               into it on every rank (requires n % g == 0).
  * All ranks pass identical n, m, p, root, ngpu.  Every output element is
  * accumulated in the same order as la_gemm (which never splits K here), so
- * results are bitwise identical to the single-GPU path without split-K.  Errors: NOT_INITIALIZED, INVALID_VALUE (ngpu !=
- * communicator size, dims), UNSUPPORTED (C_full with n % g != 0), NCCL, CUDA. */
+ * results are bitwise identical to the single-GPU path without split-K.
+ * Errors: NOT_INITIALIZED, INVALID_VALUE (ngpu != communicator size, dims),
+ * UNSUPPORTED (C_full with n % g != 0), NCCL, CUDA. */
 LA_API la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
                         const float *d_B, float *d_C_local, float *d_C_full, int root,
                         int ngpu, void *stream);
