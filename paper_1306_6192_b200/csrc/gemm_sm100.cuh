@@ -8,21 +8,26 @@
 //   * staging      : TMA (cp.async.bulk.tensor) fills a STAGES-deep ring of
 //                    128B-swizzled K-major tiles; mbarrier full[s] replaces the
 //                    first __syncthreads;
-//   * inner product: one elected thread issues tcgen05.mma.kind::tf32 into a
-//                    TMEM accumulator (3 passes hi.lo', lo.hi', hi.hi' per K=8
-//                    step for 3xTF32); tcgen05.commit -> empty[s] replaces the
+//   * inner product: the MMA warp, converged, with one lane elected inside each
+//                    asm statement and every descriptor on the uniform
+//                    datapath, issues tcgen05.mma.kind::tf32 into a TMEM
+//                    accumulator (3 passes hi.lo', lo.hi', hi.hi' per K=8 step
+//                    for 3xTF32); tcgen05.commit -> empty[s] replaces the
 //                    second __syncthreads;
 //   * write-back   : epilogue warps tcgen05.ld the accumulator and store C
-//                    exactly once per element, coalesced through a
-//                    per-warp smem transpose, 64-bit offsets, ragged edges
-//                    predicated.
+//                    exactly once per element: 32x32 pieces laid out
+//                    in swizzled smem and written by TMA bulk tensor stores
+//                    (ragged edges clipped by the hardware), or per-thread
+//                    coalesced stores for non-plain layouts (complex interleave,
+//                    fused gather); 64-bit offsets.
 // Accumulator promotion: the tcgen05 tf32 path sums each K=8 group exactly and
 // then TRUNCATES into the fp32 accumulator (measured, tests/test_probe.py), a
 // bias that grows with the number of MMAs per accumulator (3.1 x 2^-20 S at
 // K=16384).  So the MMA warp accumulates `kc` K-blocks per TMEM chunk and the
 // epilogue adds every chunk into an fp32 round-to-nearest register running
-// sum (0.06 x 2^-20 S at kc = 8 blocks of 32).  Two TMEM accumulator buffers
-// let the epilogue of chunk c overlap the MMAs of chunk c+1.
+// sum (0.06 x 2^-20 S at chunks of 256; the host picks 64 / 128 / 256 by K,
+// because one long chunk's truncations do not average out).  Two TMEM
+// accumulator buffers let the epilogue of chunk c overlap the MMAs of c+1.
 //
 // CG == 1: one CTA computes a 128 x BN tile (UMMA M=128).
 // CG == 2: a cluster of two CTAs (a CTA pair on one TPC) computes a 256 x BN
