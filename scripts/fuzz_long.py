@@ -24,6 +24,9 @@ la.init(0)
 t_end = time.time() + seconds
 cases = fails = 0
 worst = {"3xtf32": 0.0, "tf32": 0.0}
+worst_case = {"3xtf32": None, "tf32": None}
+kmin = int(os.environ.get("FUZZ_KMIN", "0"))
+kmax = int(os.environ.get("FUZZ_KMAX", "0"))
 while time.time() < t_end:
     dims = []
     for _ in range(3):
@@ -33,6 +36,8 @@ while time.time() < t_end:
             d = int(np.exp(rng.uniform(0, np.log(3000))))
         dims.append(max(1, d))
     n, m, p = dims
+    if kmax:  # targeted K range
+        m = int(rng.integers(kmin, kmax + 1))
     seed = int(rng.integers(1, 2 ** 31))
     kind = rng.choice(["stress", "random", "integer"])
     mode = "tf32" if rng.random() < 0.25 else "3xtf32"
@@ -73,8 +78,11 @@ while time.time() < t_end:
         err = float((np.abs(C.astype(np.float64) - ref) / np.maximum(S, 1e-300)).max())
         bound = 2.0 ** -20 if mode == "3xtf32" else 2.0 ** -9
         ok = err <= bound
-        worst[mode] = max(worst[mode], err / bound)
+        if err / bound > worst[mode]:
+            worst[mode] = err / bound
+            worst_case[mode] = (n, m, p, str(kind), seed)
     if not ok:
         fails += 1
         print(f"FAIL n={n} m={m} p={p} kind={kind} mode={mode} seed={seed} err={err}", flush=True)
-print(f"{cases} cases, {fails} failures; worst error / bound: 3xtf32 {worst['3xtf32']:.3f}, tf32 {worst['tf32']:.3f}")
+print(f"{cases} cases, {fails} failures; worst error / bound: 3xtf32 {worst['3xtf32']:.3f} at {worst_case['3xtf32']}, "
+      f"tf32 {worst['tf32']:.3f} at {worst_case['tf32']}")

@@ -1,7 +1,22 @@
-import os, sys, statistics, torch
-sys.path.insert(0, os.getcwd())
-import inputs, paper_1306_6192_b200 as la
+#!/usr/bin/env python
+"""Device time per call (CUDA graph of 20 calls) for promotion intervals
+(LA_OPT_PROMOTE_K) on short-K shapes, where the interval matters most.
+
+    python scripts/promote_cost.py [pk ...]"""
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import inputs  # noqa: E402
+import paper_1306_6192_b200 as la  # noqa: E402
+
 la.init(0)
+pks = [int(x) for x in sys.argv[1:]] or [-1, 64, 128, 256]
+
+
 def graph_time(n, m, p, calls=20):
     A, B = inputs.pair(n, m, p, "random", device="cuda")
     C = torch.empty(n, p, device="cuda")
@@ -13,16 +28,24 @@ def graph_time(n, m, p, calls=20):
     with torch.cuda.graph(g, stream=s):
         for _ in range(calls):
             la.gemm(A, B, out=C, stream=s)
-    g.replay(); torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
     ts = []
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) / calls * 1e3)
     return statistics.median(ts)
-for shape in [(256, 256, 256), (4096, 256, 4096), (4096, 512, 4096), (4096, 1024, 4096), (8192, 1024, 8192)]:
-    r = []
-    for pk in (-1, 256):
+
+
+for shape in [(256, 256, 256), (2048, 256, 2048), (4096, 256, 4096), (8192, 256, 8192), (2048, 512, 2048),
+              (4096, 512, 4096), (8192, 512, 8192), (4096, 1024, 4096)]:
+    row = []
+    for pk in pks:
         la.set_option("promote_k", pk)
-        r.append(graph_time(*shape))
-    print(shape, f"auto {r[0]:.1f} us  fixed-256 {r[1]:.1f} us  ({100 * (r[0] / r[1] - 1):+.1f}%)", flush=True)
+        row.append(f"pk={pk}: {graph_time(*shape):8.1f} us")
+    print(shape, " | ".join(row), flush=True)
+la.set_option("promote_k", -1)
