@@ -78,8 +78,8 @@ typedef enum {
     /* 3xTF32 only: K elements accumulated in tensor memory before the partial
      * sum is added into an fp32 register running sum (round-to-nearest).  0 =
      * never (the whole K range accumulates in TMEM); > 0: that many, rounded up
-     * to a multiple of 32.  Default -1 (automatic): 64 for K <= 192, 128 for
-     * K <= 1024, 256 beyond -- the tcgen05 tf32 accumulator truncates at every
+     * to a multiple of 32.  Default -1 (automatic): 32 for K <= 64, 64 for
+     * K <= 192, 128 for K <= 1024, 256 beyond -- the tcgen05 tf32 accumulator truncates at every
      * MMA, and one long chunk breaks the 2^-20 bound. */
     LA_OPT_PROMOTE_K = 0,
     /* Upper bound on the number of SMs the GEMM kernel occupies (0 = all).  The

@@ -315,12 +315,14 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // many chunks (RN running sum), short K does not.  Measured worst case on
     // random-sign inputs vs the exact product (scripts/positive_check.py):
     // K = 256 in one chunk 0.79 x 2^-20 S, in two of 128 0.39, in four of 64
-    // 0.19; so chunks of 64 up to K = 192, 128 up to K = 1024, 256 beyond
+    // 0.19; so chunks of 32 up to K = 64 (24-bit inputs at K = 61: 0.58 in one
+    // chunk, 0.27 in two), 64 up to K = 192, 128 up to K = 1024, 256 beyond
     // (where a finer interval costs 9-24% of throughput and buys nothing on
-    // these inputs).  Chunks of 64 cost ~18% at K = 256 (scripts/promote_cost.py).
+    // these inputs).  Chunks of 64 cost ~18% at K = 256, of 32 ~12% at K = 64
+    // on 4096-wide outputs (scripts/promote_cost.py).
     int64_t pk = PASSES == 3 ? g_state.promote_k : 0;
     const int64_t km = out.policy_k > 0 ? out.policy_k : m;
-    if (pk < 0) pk = km <= 192 ? 64 : (km <= 1024 ? 128 : 256);
+    if (pk < 0) pk = km <= 64 ? 32 : (km <= 192 ? 64 : (km <= 1024 ? 128 : 256));
     args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + KB - 1) / KB);
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);

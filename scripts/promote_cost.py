@@ -41,8 +41,11 @@ def graph_time(n, m, p, calls=20):
     return statistics.median(ts)
 
 
-for shape in [(256, 256, 256), (2048, 256, 2048), (4096, 256, 4096), (8192, 256, 8192), (2048, 512, 2048),
-              (4096, 512, 4096), (8192, 512, 8192), (4096, 1024, 4096)]:
+SHAPES = [(256, 256, 256), (2048, 256, 2048), (4096, 256, 4096), (8192, 256, 8192), (2048, 512, 2048),
+          (4096, 512, 4096), (8192, 512, 8192), (4096, 1024, 4096)]
+if os.environ.get("SHAPES"):  # e.g. SHAPES="4096x64x4096,1024x61x859"
+    SHAPES = [tuple(int(v) for v in x.split("x")) for x in os.environ["SHAPES"].split(",")]
+for shape in SHAPES:
     row = []
     for pk in pks:
         la.set_option("promote_k", pk)
