@@ -264,14 +264,15 @@ static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const floa
 
 // Split-K factor for a launch of `tiles` output tiles over `slots` concurrent
 // clusters: only with few tiles (at most half the slots) and a long K, at least
-// 8 K-blocks per piece, at most 16 pieces.
+// 8 K-blocks per piece, at most 64 pieces (S * tiles <= slots bounds the
+// partial workspace by slots x one tile, whatever S is).
 static int splitk_factor(int64_t tiles, int64_t slots, int num_kb) {
     if (const char *e = getenv("LA_SPLIT_K")) {
         const int v = atoi(e);
         if (v >= 0) return v <= 1 ? 1 : v;
     }
     if (2 * tiles > slots || num_kb < 16) return 1;
-    int S = (int)std::min<int64_t>(std::min<int64_t>(slots / tiles, num_kb / 8), 16);
+    int S = (int)std::min<int64_t>(std::min<int64_t>(slots / tiles, num_kb / 8), 64);
     if (S <= 1) return 1;
     const int per = (num_kb + S - 1) / S;
     return (num_kb + per - 1) / per;

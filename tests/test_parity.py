@@ -471,3 +471,19 @@ def test_same_sign_inputs_as_accurate_as_listing1(la, m):
     gpu = float((np.abs(C - E) / S).max())
     ref = float((np.abs(O - E) / S).max())
     assert gpu <= ref + 2.0 ** -20, (gpu / 2.0 ** -20, ref / 2.0 ** -20)
+
+
+def test_finalize_and_reinit(la):
+    """la_finalize releases everything; the library initialises again and
+    computes the same product (state, pools, streams, events rebuilt)."""
+    A, B = inputs.pair(300, 500, 200, "integer", device="cuda")
+    before = la.gemm(A, B)
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    host_before = la.gemm_host(Ah, Bh)
+    torch.cuda.synchronize()
+    la.finalize()
+    la.init(0)
+    after = la.gemm(A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(before, after)
+    assert np.array_equal(la.gemm_host(Ah, Bh), host_before)
