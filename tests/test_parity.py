@@ -487,3 +487,23 @@ def test_finalize_and_reinit(la):
     torch.cuda.synchronize()
     assert torch.equal(before, after)
     assert np.array_equal(la.gemm_host(Ah, Bh), host_before)
+
+
+def test_host_paths_tf32_mode(la, monkeypatch):
+    """Plain TF32 mode through la_gemm_host and la_gemm_host_batch (count 1 and
+    2): bitwise equal to la_gemm in the same mode."""
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    n, m, p = 2300, 700, 2100
+    A, B = inputs.pair(n, m, p, "stress", device="cuda")
+    la.set_mode("tf32")
+    try:
+        ref = la.gemm(A, B).cpu()
+        Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
+        one = la.gemm_host(Ah, Bh)
+        single = la.gemm_host_batch([Ah], [Bh])
+        two = la.gemm_host_batch([Ah, Ah], [Bh, Bh])
+    finally:
+        la.set_mode("3xtf32")
+    assert np.array_equal(one, ref.numpy())
+    assert np.array_equal(single[0], ref.numpy())
+    assert all(np.array_equal(x, ref.numpy()) for x in two)
