@@ -1059,11 +1059,18 @@ la_status la_cgemm(int64_t n, int64_t m, int64_t p, const float *d_A, const floa
         if (gb.y > 65535) return fail(LA_ERR_UNSUPPORTED, "m too large for the split grid");
         const float2 *a2 = reinterpret_cast<const float2 *>(d_A);
         const float2 *b2 = reinterpret_cast<const float2 *>(d_B);
+        // even m and a 16-byte aligned A: the vectorised A split (pairs of elements)
+        const bool avec = m % 2 == 0 && (reinterpret_cast<uintptr_t>(d_A) & 15) == 0;
+        const int blocks_a = (int)std::max<int64_t>(1, std::min<int64_t>((n * (m / 2) + 255) / 256,
+                                                                          (int64_t)g_state.sms * 8));
+        const float4 *a4 = reinterpret_cast<const float4 *>(d_A);
         if (passes == 3) {
-            split_complex_a_kernel<3><<<ga, 256, 0, st>>>(a2, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            if (avec) split_complex_a_vec_kernel<3><<<blocks_a, 256, 0, st>>>(a4, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            else split_complex_a_kernel<3><<<ga, 256, 0, st>>>(a2, ops.a_hi, ops.a_lo, n, m, ops.mp);
             split_complex_b_kernel<3><<<gb, dim3(32, 8), 0, st>>>(b2, ops.b_hi, ops.b_lo, m, p, ops.mp);
         } else {
-            split_complex_a_kernel<1><<<ga, 256, 0, st>>>(a2, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            if (avec) split_complex_a_vec_kernel<1><<<blocks_a, 256, 0, st>>>(a4, ops.a_hi, ops.a_lo, n, m, ops.mp);
+            else split_complex_a_kernel<1><<<ga, 256, 0, st>>>(a2, ops.a_hi, ops.a_lo, n, m, ops.mp);
             split_complex_b_kernel<1><<<gb, dim3(32, 8), 0, st>>>(b2, ops.b_hi, ops.b_lo, m, p, ops.mp);
         }
         launches += 2;

@@ -232,6 +232,37 @@ __global__ void __launch_bounds__(256) split_complex_a_kernel(const float2 *__re
     }
 }
 
+// Same for even m: grid-stride over pairs of complex elements (16-byte loads,
+// 8-byte stores); the padding columns [2m, Kp) of both rows are zero-filled by
+// the first Kp - 2m threads of each row pair's last element.
+template <int PASSES>
+__device__ __forceinline__ void split_store2(float x0, float x1, float *hi, float *lo, int64_t off) {
+    const float h0 = ptx::to_tf32_rna(x0), h1 = ptx::to_tf32_rna(x1);
+    *reinterpret_cast<float2 *>(hi + off) = make_float2(h0, h1);
+    if constexpr (PASSES == 3)
+        *reinterpret_cast<float2 *>(lo + off) = make_float2(lo_part(x0, h0, false), lo_part(x1, h1, false));
+}
+template <int PASSES>
+__global__ void __launch_bounds__(256) split_complex_a_vec_kernel(const float4 *__restrict__ a, float *__restrict__ hi,
+                                                                  float *__restrict__ lo, int64_t n, int64_t m,
+                                                                  int64_t kp) {
+    const int64_t half = m / 2, total = n * half;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / half, k = 2 * (i - r * half);
+        const float4 v = __ldcs(a + i);  // (ar_k, ai_k, ar_k+1, ai_k+1)
+        const int64_t top = r * kp, bot = (n + r) * kp;
+        split_store2<PASSES>(v.x, v.z, hi, lo, top + k);
+        split_store2<PASSES>(-v.y, -v.w, hi, lo, top + m + k);
+        split_store2<PASSES>(v.y, v.w, hi, lo, bot + k);
+        split_store2<PASSES>(v.x, v.z, hi, lo, bot + m + k);
+        if (k == m - 2)
+            for (int64_t c = 2 * m; c < kp; c++) {
+                split_store<PASSES>(0.0f, hi, lo, top + c);
+                split_store<PASSES>(0.0f, hi, lo, bot + c);
+            }
+    }
+}
+
 // B (m x p complex) -> Bt (p x Kp): Bt[j][k] = Br[k][j], Bt[j][m + k] = Bi[k][j],
 // columns [2m, Kp) zero.  32x32 complex tiles through smem; block (32, 8).
 template <int PASSES>
