@@ -20,6 +20,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
     qs = sys.argv[2:] or ["1", "4", "8", "16", "32"]  # "q" or "q:tail_split"
     la.init(0)
+    la.set_mode(os.environ.get("E2E_MODE", "3xtf32"))
     A, B = inputs.pair(n, n, n, "random", device="cuda")
     os.environ["LA_SPLIT_K"] = "0"
     ref = la.gemm(A, B)
