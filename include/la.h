@@ -90,7 +90,12 @@ typedef enum {
     /* 1: record CUDA events around every split and GEMM launch so that
      * la_kernel_times() can report their device durations (bench.py's
      * roofline).  0 (default): no events. */
-    LA_OPT_KERNEL_TIMING = 3
+    LA_OPT_KERNEL_TIMING = 3,
+    /* SMs left to NCCL while la_gemm_multi's B panels are in flight (0..64,
+     * default 8): the communicator is created with ncclConfig_t.maxCTAs = this
+     * value (read by la_comm_init) and every GEMM launch but the last panel's
+     * runs on the remaining SMs.  Takes effect at the next la_comm_init. */
+    LA_OPT_NCCL_SMS = 4
 } la_option;
 
 /* Bind the (process-wide) library state to CUDA device `device`, check that it

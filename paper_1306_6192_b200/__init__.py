@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_PKG, "libla.so")
 LA_OK, LA_ERR_INVALID_VALUE, LA_ERR_NOT_INITIALIZED, LA_ERR_UNSUPPORTED, \
     LA_ERR_OUT_OF_MEMORY, LA_ERR_CUDA, LA_ERR_NCCL = range(7)
 MODES = {"3xtf32": 0, "tf32": 1}
-OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3}
+OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3, "nccl_sms": 4}
 
 # every symbol include/la.h declares (checked by tests/test_abi.py)
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
@@ -132,12 +132,18 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _check_dev(t, name):
+def _check_dev(t, name, dtype=None, shape=None):
+    """A contiguous 2-D CUDA tensor of `dtype` (default float32) and, if given,
+    exactly `shape`: the library trusts the sizes it is passed, so a wrong-sized
+    buffer must be rejected here, before it becomes an out-of-bounds write."""
     import torch
-    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
-        raise TypeError(f"{name} must be a float32 CUDA tensor")
+    dtype = torch.float32 if dtype is None else dtype
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype:
+        raise TypeError(f"{name} must be a {dtype} CUDA tensor")
     if t.dim() != 2 or not t.is_contiguous():
         raise ValueError(f"{name} must be a contiguous 2-D (row-major) matrix")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
 
 
 def gemm(A, B, out=None, stream=None):
@@ -152,9 +158,7 @@ def gemm(A, B, out=None, stream=None):
     if out is None:
         out = torch.empty((n, p), dtype=torch.float32, device=A.device)
     else:
-        _check_dev(out, "out")
-        if tuple(out.shape) != (n, p):
-            raise ValueError("out has the wrong shape")
+        _check_dev(out, "out", shape=(n, p))
     _check(_lib.la_gemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_gemm")
     return out
 
@@ -162,17 +166,16 @@ def gemm(A, B, out=None, stream=None):
 def cgemm(A, B, out=None, stream=None):
     """C = A . B for complex64 CUDA tensors (la_cgemm, Table 2 "Complex Float")."""
     import torch
-    for t, nm in ((A, "A"), (B, "B")):
-        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.complex64:
-            raise TypeError(f"{nm} must be a complex64 CUDA tensor")
-        if t.dim() != 2 or not t.is_contiguous():
-            raise ValueError(f"{nm} must be a contiguous 2-D (row-major) matrix")
+    _check_dev(A, "A", torch.complex64)
+    _check_dev(B, "B", torch.complex64)
     n, m = A.shape
     m2, p = B.shape
     if m != m2:
         raise ValueError("inner dimension mismatch")
     if out is None:
         out = torch.empty((n, p), dtype=torch.complex64, device=A.device)
+    else:
+        _check_dev(out, "out", torch.complex64, (n, p))
     _check(_lib.la_cgemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_cgemm")
     return out
 
@@ -180,17 +183,16 @@ def cgemm(A, B, out=None, stream=None):
 def dgemm(A, B, out=None, stream=None):
     """C = A . B for float64 CUDA tensors (la_dgemm, Table 2 "Double")."""
     import torch
-    for t, nm in ((A, "A"), (B, "B")):
-        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
-            raise TypeError(f"{nm} must be a float64 CUDA tensor")
-        if t.dim() != 2 or not t.is_contiguous():
-            raise ValueError(f"{nm} must be a contiguous 2-D (row-major) matrix")
+    _check_dev(A, "A", torch.float64)
+    _check_dev(B, "B", torch.float64)
     n, m = A.shape
     m2, p = B.shape
     if m != m2:
         raise ValueError("inner dimension mismatch")
     if out is None:
         out = torch.empty((n, p), dtype=torch.float64, device=A.device)
+    else:
+        _check_dev(out, "out", torch.float64, (n, p))
     _check(_lib.la_dgemm(n, m, p, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream_ptr(stream)), "la_dgemm")
     return out
 
@@ -205,7 +207,7 @@ def add(A, B, out=None, subtract=False, stream=None):
     if out is None:
         out = torch.empty_like(A)
     else:
-        _check_dev(out, "out")
+        _check_dev(out, "out", shape=tuple(A.shape))
     r, c = A.shape
     _check(_lib.la_add(r, c, A.data_ptr(), B.data_ptr(), out.data_ptr(), int(bool(subtract)),
                        _stream_ptr(stream)), "la_add")
@@ -283,6 +285,9 @@ def shard_rows(n: int, rank: int, ngpu: int):
     return r0.value, r.value
 
 
+_COMM = {}   # this process's rank in the library communicator (binding-side shape checks)
+
+
 def get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.la_get_unique_id(buf), "la_get_unique_id")
@@ -294,6 +299,7 @@ def comm_init(uid: bytes, rank: int, ngpu: int) -> None:
         raise ValueError("the NCCL unique id is 128 bytes")
     buf = ctypes.create_string_buffer(uid, 128)
     _check(_lib.la_comm_init(buf, int(rank), int(ngpu)), "la_comm_init")
+    _COMM.update(rank=int(rank), ngpu=int(ngpu))
 
 
 def bootstrap_unique_id(group=None) -> bytes:
@@ -338,9 +344,20 @@ def gather_buffer(n: int, p: int):
 
 
 def gemm_multi(n, m, p, A_local, B, C_local, C_full=None, root=0, ngpu=1, stream=None):
-    """la_gemm_multi: row-sharded product; B is read on `root` only."""
-    _check_dev(A_local, "A_local")
-    _check_dev(C_local, "C_local")
+    """la_gemm_multi: row-sharded product; B is read on `root` only.  A_local
+    and C_local hold this rank's rows (la_shard_rows), B is m x p (required on
+    the root, ignored elsewhere), C_full (optional) is n x p."""
+    # shapes are checked against this rank's shard when the call is consistent
+    # with the communicator; an inconsistent call is left to the library to
+    # reject (LA_ERR_INVALID_VALUE / NOT_INITIALIZED)
+    rank = _COMM.get("rank")
+    rows = shard_rows(n, rank, ngpu)[1] if rank is not None and ngpu == _COMM.get("ngpu") and n >= ngpu else None
+    _check_dev(A_local, "A_local", shape=None if rows is None else (rows, m))
+    _check_dev(C_local, "C_local", shape=None if rows is None else (rows, p))
+    if B is not None:
+        _check_dev(B, "B", shape=(m, p))
+    if C_full is not None:
+        _check_dev(C_full, "C_full", shape=(n, p))
     b = 0 if B is None else B.data_ptr()
     cf = 0 if C_full is None else C_full.data_ptr()
     _check(_lib.la_gemm_multi(n, m, p, A_local.data_ptr(), b, C_local.data_ptr(), cf, int(root), int(ngpu),

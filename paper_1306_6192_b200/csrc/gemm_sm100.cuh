@@ -86,8 +86,7 @@ struct GemmArgs {
     // and a reduction kernel sums the ksplit partials in order.  ksplit == 1: off.
     int32_t ksplit, kb_per;
     float *partial;
-    int32_t use_clc;    // 1: one cluster per tile + cluster launch control; 0: static persistent stride
-    int32_t *wave_sync; // static stride only, optional: arrival counters (zeroed per launch), one per
+    int32_t *wave_sync; // optional: arrival counters (zeroed per launch), one per
                         // (wave, K phase of sync_kb K-blocks)
     int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
     int32_t wave_slots; // counters in wave_sync; wave_sync[wave_slots] is the give-up flag
@@ -208,7 +207,7 @@ struct GemmCfg {
     static constexpr int B_ATOM = B_ROWS * ATOM_K * 4;
     static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);  // per CTA
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * 32 * 32 * 4; // per-warp transpose buffers
-    static constexpr int BAR_BYTES = 512;  // mbarriers, TMEM address, tile ids; CLC response at +256
+    static constexpr int BAR_BYTES = 512;  // mbarriers, TMEM address, tile ids; gather peer bases at +320
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
     static constexpr int COLS_PER_WARP = BN / 2;   // epilogue column half
@@ -342,10 +341,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint64_t *tempty = tfull + 2;
     uint64_t *sfull = tempty + 2;              // [SCHED_SLOTS] tile id ready (each CTA)
     uint64_t *sempty = sfull + SCHED_SLOTS;    // [SCHED_SLOTS] tile id consumed (leader)
-    uint64_t *clc_bar = sempty + SCHED_SLOTS;  // cluster-launch-control response ready
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(clc_bar + 1);
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(sempty + SCHED_SLOTS);
     int32_t *stile = reinterpret_cast<int32_t *>(tmem_holder + 4);         // [SCHED_SLOTS]
-    uint8_t *clc_resp = reinterpret_cast<uint8_t *>(full) + 256;          // 16 B, 16-B aligned
     float **gbase = reinterpret_cast<float **>(reinterpret_cast<uint8_t *>(full) + 320);  // [MAX_GATHER_PEERS]
 
     const uint32_t warp = ptx::warp_id();
@@ -379,7 +376,6 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&sfull[i], 1);                              // scheduler's remote arrive
             ptx::mbar_init(&sempty[i], CG + 1 + CG * NUM_EPI_WARPS);  // producers, MMA, epilogue warps
         }
-        ptx::mbar_init(clc_bar, 1);
         if (args.gather_win != nullptr)
             for (int pe = 0; pe < args.gather_peers; pe++)
                 gbase[pe] = static_cast<float *>(
@@ -457,14 +453,11 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 3 && rank == 0) {
         // ======================= tile scheduler (leader CTA) =======================
-        // Hands tile ids to every role of both CTAs through the sfull/sempty
-        // ring.  With use_clc the grid has one cluster per tile: the first tile
-        // is this cluster's own, later ones are claimed by cancelling clusters
-        // the hardware has not launched yet (cluster launch control), so the
-        // tiles in flight stay a compact window of the raster order (L2 reuse)
-        // and faster SM pairs simply take more tiles.
+        // Hands work-item ids to every role of both CTAs through the
+        // sfull/sempty ring: a static stride over the items in grouped raster
+        // order (each cluster takes items cluster_id, + num_clusters, ...).
         int slot = 0;
-        uint32_t ph = 0, cph = 0;
+        uint32_t ph = 0;
         int t = cluster_id;
         for (;;) {
             if (t >= num_items) t = -1;
@@ -479,19 +472,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             __syncwarp();
             if (++slot == SCHED_SLOTS) { slot = 0; ph ^= 1; }
             if (t < 0) break;
-            if (args.use_clc) {
-                if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(clc_bar, 16);
-                    ptx::clc_try_cancel(clc_resp, clc_bar);
-                }
-                __syncwarp();
-                ptx::mbar_wait(clc_bar, cph);
-                cph ^= 1;
-                const int32_t x = ptx::clc_query(clc_resp);
-                t = x < 0 ? -1 : x / CG;
-            } else {
-                t += num_clusters;
-            }
+            t += num_clusters;
         }
     } else if (warp == 1 && rank == 0) {
         // ======================= MMA issuer (leader CTA) =======================

@@ -42,6 +42,20 @@ la_status fail(la_status s, const char *fmt, ...) {
     return s;
 }
 
+int64_t test_hook(const char *name, int64_t dflt) {
+    const char *e = getenv(name);
+    return e && *e ? atoll(e) : dflt;
+}
+
+int64_t diag_knob(const char *name, int64_t dflt) {
+#ifdef LA_DIAGNOSTICS
+    return test_hook(name, dflt);
+#else
+    (void)name;
+    return dflt;
+#endif
+}
+
 la_status cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
     return fail(LA_ERR_CUDA, "%s failed: %s (%s) at %s:%d", what, cudaGetErrorName(e),
                 cudaGetErrorString(e), file, line);
@@ -175,10 +189,7 @@ Operands operands_carve(void *ws, int64_t n, int64_t m, int64_t p, int passes) {
     return o;
 }
 
-static bool lo_raw() { return getenv("LA_LO_RAW") && atoi(getenv("LA_LO_RAW")) != 0; }  // A/B knob
-
 la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cudaStream_t st, int *launches) {
-    const bool raw = lo_raw();
     cudaEvent_t t0;
     la_status ts = timing_begin(st, &t0);
     if (ts != LA_OK) return ts;
@@ -188,17 +199,17 @@ la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cud
         if (ops.passes == 3)
             split_rows_vec4_kernel<3><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
                                                               reinterpret_cast<float4 *>(ops.a_hi),
-                                                              reinterpret_cast<float4 *>(ops.a_lo), count4, raw);
+                                                              reinterpret_cast<float4 *>(ops.a_lo), count4);
         else
             split_rows_vec4_kernel<1><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
                                                               reinterpret_cast<float4 *>(ops.a_hi),
-                                                              reinterpret_cast<float4 *>(ops.a_lo), count4, raw);
+                                                              reinterpret_cast<float4 *>(ops.a_lo), count4);
     } else {
         dim3 grid((unsigned)std::min<int64_t>((ops.mp + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
         if (ops.passes == 3)
-            split_rows_kernel<3><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp, raw);
+            split_rows_kernel<3><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp);
         else
-            split_rows_kernel<1><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp, raw);
+            split_rows_kernel<1><<<grid, 256, 0, st>>>(A, ops.a_hi, ops.a_lo, n, m, ops.mp);
     }
     (*launches)++;
     cudaError_t e = cudaGetLastError();
@@ -216,17 +227,17 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
     if (ts != LA_OK) return ts;
     float *hi = ops.b_hi + j0 * ops.mp, *lo = ops.b_lo + j0 * ops.mp;
     const bool vec = pc % 4 == 0 && ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0;
-    const bool T64 = vec && !(getenv("LA_SPLIT_T32") && atoi(getenv("LA_SPLIT_T32")) != 0);  // A/B knob
+    const bool T64 = vec && diag_knob("LA_SPLIT_T32", 0) == 0;
     if (T64) {
         dim3 g64((unsigned)((pc + 63) / 64), (unsigned)((ops.mp + 63) / 64));
         if (ops.passes == 3)
-            split_transpose64_kernel<3><<<g64, 256, 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
+            split_transpose64_kernel<3><<<g64, 256, 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
         else
-            split_transpose64_kernel<1><<<g64, 256, 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
+            split_transpose64_kernel<1><<<g64, 256, 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
     } else if (ops.passes == 3)
-        split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
+        split_transpose_kernel<3><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
     else
-        split_transpose_kernel<1><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp, lo_raw());
+        split_transpose_kernel<1><<<grid, dim3(32, 8), 0, st>>>(b, hi, lo, m, pc, ldb, ops.mp);
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "split_b launch", __FILE__, __LINE__);
@@ -237,9 +248,9 @@ la_status split_b(int64_t m, int64_t j0, int64_t pc, const float *B, int64_t ldb
 // vectorised transpose; returns false (nothing launched) otherwise.
 static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const Operands &ops,
                      cudaStream_t st, int *launches, la_status *status) {
-    const bool t32 = getenv("LA_SPLIT_T32") && atoi(getenv("LA_SPLIT_T32")) != 0;
+    const bool t32 = diag_knob("LA_SPLIT_T32", 0) != 0;
     if (m % 4 || p % 4 || ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) || t32 ||
-        (getenv("LA_SPLIT_SEPARATE") && atoi(getenv("LA_SPLIT_SEPARATE")) != 0))
+        test_hook("LA_SPLIT_SEPARATE", 0) != 0)
         return false;
     const int64_t count4 = n * m / 4;
     const int64_t na = std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, (int64_t)g_state.sms * 8));
@@ -251,11 +262,9 @@ static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const floa
     const float4 *a4 = reinterpret_cast<const float4 *>(A);
     float4 *ah = reinterpret_cast<float4 *>(ops.a_hi), *al = reinterpret_cast<float4 *>(ops.a_lo);
     if (ops.passes == 3)
-        split_ab_kernel<3><<<grid, 256, 0, st>>>(a4, ah, al, count4, na, B, ops.b_hi, ops.b_lo, m, p, ops.mp, nbx,
-                                                 lo_raw());
+        split_ab_kernel<3><<<grid, 256, 0, st>>>(a4, ah, al, count4, na, B, ops.b_hi, ops.b_lo, m, p, ops.mp, nbx);
     else
-        split_ab_kernel<1><<<grid, 256, 0, st>>>(a4, ah, al, count4, na, B, ops.b_hi, ops.b_lo, m, p, ops.mp, nbx,
-                                                 lo_raw());
+        split_ab_kernel<1><<<grid, 256, 0, st>>>(a4, ah, al, count4, na, B, ops.b_hi, ops.b_lo, m, p, ops.mp, nbx);
     (*launches)++;
     cudaError_t e = cudaGetLastError();
     *status = e != cudaSuccess ? cuda_fail(e, "split_ab launch", __FILE__, __LINE__) : timing_end(st, t0, TIMED_SPLIT);
@@ -267,10 +276,8 @@ static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const floa
 // 8 K-blocks per piece, at most 64 pieces (S * tiles <= slots bounds the
 // partial workspace by slots x one tile, whatever S is).
 static int splitk_factor(int64_t tiles, int64_t slots, int num_kb) {
-    if (const char *e = getenv("LA_SPLIT_K")) {
-        const int v = atoi(e);
-        if (v >= 0) return v <= 1 ? 1 : v;
-    }
+    const int64_t forced = test_hook("LA_SPLIT_K", -1);
+    if (forced >= 0) return forced <= 1 ? 1 : (int)std::min<int64_t>(forced, 1024);
     if (2 * tiles > slots || num_kb < 16) return 1;
     int S = (int)std::min<int64_t>(std::min<int64_t>(slots / tiles, num_kb / 8), 64);
     if (S <= 1) return 1;
@@ -328,13 +335,14 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
-    const int group_env = getenv("LA_GROUP_M") ? atoi(getenv("LA_GROUP_M")) : 0;  // experiment knob
-    args.group_m = group_env > 0 ? group_env : 8;
+    args.group_m = (int32_t)std::max<int64_t>(1, diag_knob("LA_GROUP_M", 8));
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
 
     auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES, KB>;
+    // per-device setup, redone after la_finalize + la_init (possibly another device)
     static int max_clusters = 0;
-    if (max_clusters == 0) {
+    static uint64_t setup_gen = 0;
+    if (setup_gen != g_state.generation) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)", __FILE__, __LINE__);
         cudaLaunchConfig_t cfg = {};
@@ -355,27 +363,18 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
             nc = g_state.sms / CG;
         }
         max_clusters = nc;
+        setup_gen = g_state.generation;
     }
-    // Default: a static persistent grid (one cluster per SM pair, tiles strided
-    // in grouped raster order).  LA_CLC=1 instead launches one cluster per tile
-    // and lets running clusters claim pending ones through cluster launch
-    // control (dynamic balancing) -- measured: 129 GB of DRAM reads per n=16384
-    // launch vs 105-113 GB static, because dynamically started tiles drift
-    // apart in K and share fewer L2 slabs (profiles/ncu_r01_sched_ab.md).  CLC
-    // is never used when the caller caps the SMs (it cannot bound residency).
+    // A static persistent grid: one cluster per SM pair, tiles strided in
+    // grouped raster order.  (A dynamic schedule through cluster launch control
+    // was measured worse -- 129 vs 105-113 GB of DRAM reads per n = 16384
+    // launch, profiles/ncu_r01_sched_ab.md -- and removed.)
     int clusters = max_clusters;
-    const bool env_clc = getenv("LA_CLC") && atoi(getenv("LA_CLC")) != 0;
-    args.use_clc = (max_sms <= 0 && env_clc) ? 1 : 0;
     if (max_sms > 0) clusters = std::min(clusters, std::max(1, max_sms / CG));
 #ifdef LA_DIAGNOSTICS
-    // energy diagnostics: fewer resident clusters with the wave barrier kept
-    if (const char *mc = getenv("LA_DIAG_CLUSTERS")) clusters = std::min(clusters, std::max(1, atoi(mc)));
+    clusters = std::min<int>(clusters, (int)std::max<int64_t>(1, diag_knob("LA_DIAG_CLUSTERS", clusters)));
 #endif
     clusters = (int)std::min<int64_t>(tiles, clusters);
-    if (args.use_clc) {
-        if (tiles * CG > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "too many tiles for one launch");
-        clusters = (int)tiles;
-    }
     // Split-K: fewer tiles than half the clusters and a long K -> each tile's K
     // range is cut into S pieces (at least 8 K-blocks each) computed by
     // different clusters; partial tiles go to a workspace and are summed in
@@ -387,7 +386,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     void *part_buf = nullptr;
     {
         const int kb32 = (int)((m + 31) / 32);
-        const int S = (out.splitk_ok && !args.use_clc) ? splitk_factor(tiles, max_clusters, kb32) : 1;
+        const int S = out.splitk_ok ? splitk_factor(tiles, max_clusters, kb32) : 1;
         if (S > 1) {
             // pieces of kb_per K-blocks; recount S from the piece size so every
             // piece is non-empty ((S - 1) * kb_per < num_kb)
@@ -414,8 +413,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // identical with or without it.  LA_TAIL_SPLIT=0 disables.
     args.full_items = args.num_items = (int32_t)(tiles * args.ksplit);
     {
-        const char *te = getenv("LA_TAIL_SPLIT");
-        const bool tail_split = !args.use_clc && args.ksplit == 1 && (te == nullptr || atoi(te) != 0);
+        const bool tail_split = args.ksplit == 1 && test_hook("LA_TAIL_SPLIT", 1) != 0;
         const int64_t W = clusters, R = tiles % W;
         if (tail_split && R > 0 && 2 * R <= W && tiles > W) {
             args.full_items = (int32_t)(tiles - R);
@@ -428,7 +426,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     memset(&tm_c, 0, sizeof tm_c);
     {
         float *base = args.ksplit > 1 ? args.partial : args.C;
-        const bool env_off = getenv("LA_TMA_STORE") && atoi(getenv("LA_TMA_STORE")) == 0;
+        const bool env_off = test_hook("LA_TMA_STORE", 1) == 0;
         args.tma_store = !env_off && out.cstride == 1 && out.half_rows == 0 && out.gather_win == nullptr &&
                          ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0 && n < ((int64_t)1 << 31) &&
                          pc < ((int64_t)1 << 31);
@@ -438,11 +436,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
 #ifdef LA_DIAGNOSTICS
     // Energy diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip
     // MMAs.  Compiled in only with LA_BUILD_DIAGNOSTICS=1 at build time.
-    args.debug = getenv("LA_DEBUG_KERNEL") ? atoi(getenv("LA_DEBUG_KERNEL")) : 0;
+    args.debug = (int32_t)diag_knob("LA_DEBUG_KERNEL", 0);
     // LA_DIAG_TRACE=1: per-CTA globaltimer stamps, printed after the launch
     // (host-synchronising; diagnostics only)
     static int64_t *trace_buf = nullptr;
-    const bool trace_on = getenv("LA_DIAG_TRACE") && atoi(getenv("LA_DIAG_TRACE")) != 0;
+    const bool trace_on = diag_knob("LA_DIAG_TRACE", 0) != 0;
     if (trace_on) {
         if (!trace_buf) cudaMalloc(&trace_buf, 8 * sizeof(int64_t) * 1024);
         cudaMemsetAsync(trace_buf, 0, 8 * sizeof(int64_t) * 1024, st);
@@ -462,15 +460,15 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // launch, 13% less energy and +14% sustained throughput under the power cap
     // (profiles/energy_r01.md).  On by default for multi-wave problems with a
     // long K; LA_WAVE_SYNC=0 disables, =N sets the interval in K-blocks.
-    const char *ws_env = getenv("LA_WAVE_SYNC");
+    const int64_t ws_env = diag_knob("LA_WAVE_SYNC", -1);
     // Never with an SM cap: the capped launch runs beside other kernels (NCCL in
     // la_gemm_multi) and every participant of a wave must be resident.
     // Default only for 3xTF32: with one TF32 pass each K phase is 3x shorter and
     // the barrier costs more than it saves (n = 8192 TF32: 660 vs 628 TFLOP/s off/on).
-    int wave_sync = ws_env ? atoi(ws_env) * BK / KB
+    int wave_sync = ws_env >= 0 ? (int)ws_env * BK / KB
                            : (PASSES == 3 && args.num_kb * KB >= 64 * BK ? 16 * BK / KB : 0);
     if (max_sms > 0 || args.ksplit > 1) wave_sync = 0;
-    if (!args.use_clc && wave_sync > 0) {
+    if (wave_sync > 0) {
         args.sync_kb = std::max(1, std::min(args.num_kb, wave_sync));
         const int64_t phases = (args.num_kb + args.sync_kb - 1) / args.sync_kb;
         const size_t nw = (size_t)((args.num_items + clusters - 1) / clusters * phases);
@@ -569,10 +567,8 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
 // (scripts/cg_choice.py): pair wins from ~40 tiles up without split-K
 // (n = 2048: 108 vs 145 us), single-CTA for tiny problems (n = 256).
 static int choose_cta_group(int64_t n, int64_t pc, int num_kb, bool splitk_ok) {
-    if (const char *e = getenv("LA_CTA_GROUP")) {
-        const int v = atoi(e);
-        if (v == 1 || v == 2) return v;
-    }
+    const int64_t forced = test_hook("LA_CTA_GROUP", 0);
+    if (forced == 1 || forced == 2) return (int)forced;
     double cost[3] = {0, 0, 0};
     for (int cg = 1; cg <= 2; cg++) {
         const int64_t tm = 128 * cg, tn = cg == 2 ? 256 : 128;
@@ -605,8 +601,8 @@ la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands 
     // pass -- measured +2.6..4.7% at n = 16384, -0.7..1.6% at n = 4096 / 8192
     // (more, smaller stages win when the clock is not capped), hence only from
     // 2^41 multiply-adds up.  LA_TF32_KB=32|64 forces either (A/B knob).
-    const char *kbe = getenv("LA_TF32_KB");
-    const bool kb64 = kbe ? atoi(kbe) == 64 : (double)n * (double)pc * (double)m >= 2199023255552.0;
+    const int64_t kbe = test_hook("LA_TF32_KB", 0);
+    const bool kb64 = kbe ? kbe == 64 : (double)n * (double)pc * (double)m >= 2199023255552.0;
     if (kb64) {
         if (cg == 2) return launch_gemm<2, 256, 3, 1, 64>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         return launch_gemm<1, 128, 3, 1, 64>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
@@ -701,7 +697,8 @@ la_status la_init(int device) {
     LA_CK(cudaMemPoolSetAttribute(g_state.pool, cudaMemPoolAttrReleaseThreshold, &thr));
     g_state.device = device;
     g_state.sms = prop.multiProcessorCount;
-    if (const char *env = getenv("LA_PROMOTE_K")) g_state.promote_k = atoll(env);
+    static uint64_t generations = 0;
+    g_state.generation = ++generations;  // invalidates per-device kernel setup cached by earlier inits
     g_state.initialized = true;
     return LA_OK;
 }
@@ -732,6 +729,10 @@ la_status la_set_option(la_option option, int64_t value) {
             if (value != 0 && value != 1) return fail(LA_ERR_INVALID_VALUE, "kernel_timing is 0 or 1");
             g_state.kernel_timing = value == 1;
             return LA_OK;
+        case LA_OPT_NCCL_SMS:
+            if (value < 0 || value > 64) return fail(LA_ERR_INVALID_VALUE, "nccl_sms must be in [0, 64]");
+            g_state.nccl_sms = value;
+            return LA_OK;
     }
     return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
 }
@@ -744,6 +745,7 @@ la_status la_get_option(la_option option, int64_t *value) {
         case LA_OPT_MAX_SMS: *value = g_state.max_sms; return LA_OK;
         case LA_OPT_PANELS: *value = g_state.panels; return LA_OK;
         case LA_OPT_KERNEL_TIMING: *value = g_state.kernel_timing ? 1 : 0; return LA_OK;
+        case LA_OPT_NCCL_SMS: *value = g_state.nccl_sms; return LA_OK;
     }
     return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
 }
@@ -794,14 +796,12 @@ struct HostTrace {
 };
 
 static int64_t host_tail_split() {
-    const char *v = getenv("LA_HOST_TAIL_SPLIT");
-    const int64_t t = v ? atoll(v) : 2;
+    const int64_t t = diag_knob("LA_HOST_TAIL_SPLIT", 2);
     return std::max<int64_t>(1, std::min<int64_t>(t, 16));
 }
 
 static int64_t host_panels() {
-    const char *v = getenv("LA_HOST_PANELS");
-    const int64_t q = v ? atoll(v) : 12;
+    const int64_t q = test_hook("LA_HOST_PANELS", 12);
     return std::max<int64_t>(1, std::min<int64_t>(q, 64));
 }
 
@@ -970,7 +970,7 @@ static la_status host_run(int64_t count, int64_t n, int64_t m, int64_t p, const 
     const Operands ops = operands_carve(ws, n, m, p, passes);
     int launches = 0;
     HostTrace tr;
-    tr.on = getenv("LA_HOST_TRACE") && atoi(getenv("LA_HOST_TRACE")) != 0;
+    tr.on = diag_knob("LA_HOST_TRACE", 0) != 0;
     cudaEvent_t ev_start = g_state.slot_events[0];
     cudaEvent_t *done_compute = &g_state.slot_events[1], *done_d2h = &g_state.slot_events[3];
     // the copy streams start after everything already queued on `st`
@@ -1108,29 +1108,29 @@ la_status la_dgemm(int64_t n, int64_t m, int64_t p, const double *d_A, const dou
     const int64_t gy = (n + DBM - 1) / DBM, gx = (p + DBN - 1) / DBN;
     if (gy > 65535 || gx > INT32_MAX) return fail(LA_ERR_UNSUPPORTED, "matrix too large for the DGEMM grid");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr_gen = 0;
+    if (attr_gen != g_state.generation) {
         cudaError_t e = cudaFuncSetAttribute(dgemm_sm100_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              DSMEM_BYTES);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(dgemm_sm100_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      DSMEM_BYTES);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(dgemm)", __FILE__, __LINE__);
-        attr = true;
+        attr_gen = g_state.generation;
     }
     const bool vec16 = m % 2 == 0 && p % 2 == 0 &&
                        ((reinterpret_cast<uintptr_t>(d_A) | reinterpret_cast<uintptr_t>(d_B)) & 15) == 0;
     // TMA path (int32 box coordinates); LA_DGEMM_CPASYNC=1 selects the cp.async kernel (A/B knob)
     const bool tma = vec16 && n < ((int64_t)1 << 31) && m < ((int64_t)1 << 31) && p < ((int64_t)1 << 31) &&
-                     !(getenv("LA_DGEMM_CPASYNC") && atoi(getenv("LA_DGEMM_CPASYNC")) != 0);
+                     test_hook("LA_DGEMM_CPASYNC", 0) == 0;
     CUtensorMap tA, tB;
     if (tma) {
-        static bool attr_tma = false;
-        if (!attr_tma) {
+        static uint64_t attr_tma_gen = 0;
+        if (attr_tma_gen != g_state.generation) {
             cudaError_t e = cudaFuncSetAttribute(dgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  DT_SMEM_BYTES);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(dgemm_tma)", __FILE__, __LINE__);
-            attr_tma = true;
+            attr_tma_gen = g_state.generation;
         }
         la_status ms;
         if ((ms = make_tmap_f64(&tA, d_A, n, m, DBM)) != LA_OK) return ms;

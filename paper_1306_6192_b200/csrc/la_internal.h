@@ -15,6 +15,7 @@ struct State {
     bool initialized = false;
     int device = -1;
     int sms = 0;
+    uint64_t generation = 0;  // bumped by every la_init: per-device setup cached in statics is redone
     cudaMemPool_t pool = nullptr;
     la_mode mode = LA_MODE_3XTF32;
     // Accumulator promotion interval in K elements (0 = whole K in TMEM).
@@ -23,6 +24,7 @@ struct State {
     int64_t promote_k = -1;  // -1: automatic by K (launch_gemm)
     int64_t max_sms = 0;
     int64_t panels = 4;
+    int64_t nccl_sms = 8;  // SMs left to NCCL (ncclConfig_t.maxCTAs) while B panels are in flight
     int last_launches = 0;
     void *staging = nullptr;  // la_gemm_host device staging
     size_t staging_bytes = 0;
@@ -42,6 +44,25 @@ extern std::recursive_mutex g_mutex;  // serialises every entry point's host-sid
 extern thread_local std::string g_last_error;
 
 la_status fail(la_status s, const char *fmt, ...);
+
+// Environment hooks, all read through these two functions.
+// Test hooks force one of several CORRECT dispatch paths, so that the tests can
+// compare the paths bitwise (always compiled; each is set by a test):
+//   LA_SPLIT_K=0|S         split-K off / forced to S pieces (tests/test_parity.py, test_multi.py)
+//   LA_TAIL_SPLIT=0        no half-width tail items            (tests/test_fuzz.py)
+//   LA_SPLIT_SEPARATE=1    two split launches instead of one   (tests/test_parity.py)
+//   LA_TMA_STORE=0         per-thread epilogue stores          (tests/test_parity.py)
+//   LA_CTA_GROUP=1|2       single-CTA or CTA-pair kernel       (tests/test_fuzz.py)
+//   LA_TF32_KB=32|64       plain-TF32 K-block width            (tests/test_parity.py)
+//   LA_HOST_PANELS=q       host transfer panels                (tests/test_parity.py)
+//   LA_DGEMM_CPASYNC=1     cp.async DGEMM instead of TMA       (tests/test_parity_ext.py)
+//   LA_TEST_GATHER_ROW0=r  fused-gather destination row, 1 rank (tests/test_multi.py)
+// Experiment knobs (LA_SPLIT_T32, LA_GROUP_M, LA_WAVE_SYNC, LA_HOST_TAIL_SPLIT,
+// LA_HOST_TRACE, LA_DIAG_CLUSTERS, LA_DIAG_TRACE, LA_DEBUG_KERNEL) are read only
+// in the diagnostics build (LA_BUILD_DIAGNOSTICS=1); elsewhere diag_knob
+// returns the default.
+int64_t test_hook(const char *name, int64_t dflt);
+int64_t diag_knob(const char *name, int64_t dflt);
 la_status cuda_fail(cudaError_t e, const char *what, const char *file, int line);
 la_status validate_gemm(int64_t n, int64_t m, int64_t p, const float *A, const float *B, const float *C);
 

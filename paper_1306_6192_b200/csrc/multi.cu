@@ -87,11 +87,9 @@ la_status comm_destroy() {
     return s;
 }
 
-// SMs left free for NCCL's kernels while broadcasts are in flight.
-static int reserved_sms() {
-    if (const char *e = getenv("LA_NCCL_RESERVED_SMS")) return std::max(0, atoi(e));
-    return 8;
-}
+// SMs left free for NCCL's kernels while broadcasts are in flight
+// (LA_OPT_NCCL_SMS, default 8; read by la_comm_init for ncclConfig_t.maxCTAs).
+static int reserved_sms() { return (int)std::max<int64_t>(0, g_state.nccl_sms); }
 
 }  // namespace la
 
@@ -160,7 +158,10 @@ la_status la_gather_alloc(int64_t bytes, void **d_out) {
     }
     g_comm.gather_bytes = sz;
     g_comm.lsa_size = ncclTeamLsa(g_comm.comm).nRanks;
-    if (!g_comm.barrier_buf) LA_CK(cudaMalloc(&g_comm.barrier_buf, sizeof(int)));
+    if (!g_comm.barrier_buf) {
+        LA_CK(cudaMalloc(&g_comm.barrier_buf, sizeof(int)));
+        LA_CK(cudaMemset(g_comm.barrier_buf, 0, sizeof(int)));
+    }
     *d_out = g_comm.gather;
     return LA_OK;
 }
@@ -220,9 +221,39 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
     const Operands ops = operands_carve(ws, rows, m, p, passes);
     int launches = 0;
 
+    // Fused all-gather: C_full is the registered symmetric window and every
+    // rank is load/store reachable (one NVLink domain) -> the epilogue writes
+    // this rank's rows into every rank's C_full while the GEMM runs, instead of
+    // a separate ncclAllGather afterwards.
+    OutSpec out;
+    const bool fused = d_C_full != nullptr && d_C_full == g_comm.gather && g_comm.gather_win != nullptr &&
+                       g_comm.lsa_size == ngpu && ngpu <= MAX_GATHER_PEERS &&
+                       (size_t)(n * p) * sizeof(float) <= g_comm.gather_bytes;
+    if (fused) {
+        out.gather_win = g_comm.gather_win;
+        out.gather_peers = g_comm.lsa_size;
+        out.gather_row0 = row0;
+        out.gather_ld = p;
+        const int64_t hook_row0 = ngpu == 1 ? test_hook("LA_TEST_GATHER_ROW0", -1) : -1;
+        if (hook_row0 >= 0) {  // test hook: exercise a non-zero destination row with one rank
+            out.gather_row0 = hook_row0;
+            if ((size_t)((out.gather_row0 + rows) * p) * sizeof(float) > g_comm.gather_bytes)
+                return fail(LA_ERR_INVALID_VALUE, "LA_TEST_GATHER_ROW0 past the gather buffer");
+        }
+    }
     // comm stream starts after everything already queued on the caller's stream
     LA_CK(cudaEventRecord(g_comm.start, st));
     LA_CK(cudaStreamWaitEvent(g_comm.stream, g_comm.start, 0));
+    if (fused && ngpu > 1) {
+        // Write-after-read guard for the fused gather: this call's epilogues store
+        // into every rank's C_full, which a rank may still be reading from the
+        // previous call (work queued on its `stream` before this call).  A 1-int
+        // all-reduce on the comm stream, which starts only after that work,
+        // holds every rank's broadcasts -- and so every GEMM, which waits for
+        // panel 0 -- until all ranks have reached this call.
+        LA_NCCL(ncclAllReduce(g_comm.barrier_buf, g_comm.barrier_buf, 1, ncclInt, ncclSum, g_comm.comm,
+                              g_comm.stream));
+    }
     for (int64_t c = 0; c < P; c++) {
         const int64_t j0 = c * pc, w = std::min(pc, p - j0);
         float *panel = bstage + m * j0;  // packed m x w panel
@@ -240,26 +271,6 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
         LA_CK(cudaEventRecord(g_comm.panel_ready[c], g_comm.stream));
     }
 
-    // Fused all-gather: C_full is the registered symmetric window and every
-    // rank is load/store reachable (one NVLink domain) -> the epilogue writes
-    // this rank's rows into every rank's C_full while the GEMM runs, instead of
-    // a separate ncclAllGather afterwards.
-    OutSpec out;
-    const bool fused = d_C_full != nullptr && d_C_full == g_comm.gather && g_comm.gather_win != nullptr &&
-                       g_comm.lsa_size == ngpu && ngpu <= MAX_GATHER_PEERS &&
-                       (size_t)(n * p) * sizeof(float) <= g_comm.gather_bytes;
-    if (fused) {
-        out.gather_win = g_comm.gather_win;
-        out.gather_peers = g_comm.lsa_size;
-        out.gather_row0 = row0;
-        out.gather_ld = p;
-        if (ngpu == 1)
-            if (const char *e = getenv("LA_TEST_GATHER_ROW0")) {  // test hook: exercise a non-zero row offset
-                out.gather_row0 = atoll(e);
-                if ((size_t)((out.gather_row0 + rows) * p) * sizeof(float) > g_comm.gather_bytes)
-                    return fail(LA_ERR_INVALID_VALUE, "LA_TEST_GATHER_ROW0 past the gather buffer");
-            }
-    }
     la_status s = split_a(rows, m, d_A_local, ops, st, &launches);
     const int reserve = ngpu > 1 ? reserved_sms() : 0;
     for (int64_t c = 0; c < P && s == LA_OK; c++) {

@@ -173,40 +173,6 @@ __device__ __forceinline__ void st_shared_cluster_u32(const void *p, uint32_t ct
         : "memory");
 }
 
-// ---------------------------------------------------------------- cluster launch control
-// Ask the hardware to cancel the launch of a cluster that has not started yet
-// and hand its work to us; the 16-byte response lands in `resp` (this CTA)
-// and completes 16 tx bytes on `bar`.
-__device__ __forceinline__ void clc_try_cancel(void *resp, uint64_t *bar) {
-    asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::
-                     "r"(smem_u32(resp)),
-                 "r"(smem_u32(bar))
-                 : "memory");
-}
-// Decode a response: returns the x coordinate of the first CTA of the
-// canceled cluster, or -1 if nothing was canceled (no cluster left to launch).
-__device__ __forceinline__ int32_t clc_query(const void *resp) {
-    uint64_t lo, hi;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(smem_u32(resp)) : "memory");
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .b128 R;\n\t.reg .pred P;\n\t"
-        "mov.b128 R, {%1, %2};\n\t"
-        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}"
-        : "=r"(ok)
-        : "l"(lo), "l"(hi));
-    if (!ok) return -1;
-    uint32_t x;
-    asm volatile(
-        "{\n\t.reg .b128 R;\n\t"
-        "mov.b128 R, {%1, %2};\n\t"
-        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %0, R;\n\t}"
-        : "=r"(x)
-        : "l"(lo), "l"(hi));
-    return (int32_t)x;
-}
-
 // ---------------------------------------------------------------- tcgen05
 template <int CG>
 __device__ __forceinline__ void tmem_alloc(uint32_t *holder, uint32_t ncols) {

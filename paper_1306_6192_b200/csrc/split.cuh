@@ -25,24 +25,21 @@ namespace la {
 // TF32 bits of its fp32 operands, so this changes lo by at most half a TF32 ulp
 // (the per-product bound improves from 2^-21.06 to 2^-21.03 for 24-bit inputs,
 // SURVEY App. A) and stops 13 dead low bits from toggling through shared memory
-// and the operand path (LA_LO_RAW=1 restores the raw residual, for A/B runs).
-__device__ __forceinline__ float lo_part(float x, float h, bool raw) {
-    const float l = x - h;
-    return raw ? l : ptx::to_tf32_rna(l);
-}
+// and the operand path.
+__device__ __forceinline__ float lo_part(float x, float h) { return ptx::to_tf32_rna(x - h); }
 
 template <int PASSES>
-__device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64_t off, bool raw = false) {
+__device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64_t off) {
     const float h = ptx::to_tf32_rna(x);
     hi[off] = h;
-    if constexpr (PASSES == 3) lo[off] = lo_part(x, h, raw);
+    if constexpr (PASSES == 3) lo[off] = lo_part(x, h);
 }
 
 // Row-major A, m % 4 == 0: flat float4 grid-stride loop (mp == m).
 template <int PASSES>
 __device__ __forceinline__ void split_rows_vec4_body(const float4 *__restrict__ a, float4 *__restrict__ hi,
                                                     float4 *__restrict__ lo, int64_t count4, int64_t block,
-                                                    int64_t nblocks, bool lo_raw) {
+                                                    int64_t nblocks) {
     for (int64_t i = block * (int64_t)blockDim.x + threadIdx.x; i < count4; i += nblocks * blockDim.x) {
         const float4 x = __ldcs(a + i);
         float4 h, l;
@@ -52,10 +49,10 @@ __device__ __forceinline__ void split_rows_vec4_body(const float4 *__restrict__ 
         h.w = ptx::to_tf32_rna(x.w);
         __stcg(hi + i, h);
         if constexpr (PASSES == 3) {
-            l.x = lo_part(x.x, h.x, lo_raw);
-            l.y = lo_part(x.y, h.y, lo_raw);
-            l.z = lo_part(x.z, h.z, lo_raw);
-            l.w = lo_part(x.w, h.w, lo_raw);
+            l.x = lo_part(x.x, h.x);
+            l.y = lo_part(x.y, h.y);
+            l.z = lo_part(x.z, h.z);
+            l.w = lo_part(x.w, h.w);
             __stcg(lo + i, l);
         }
     }
@@ -65,9 +62,9 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_rows_vec4_kernel(const float4 *__restrict__ a,
                                                               float4 *__restrict__ hi,
                                                               float4 *__restrict__ lo,
-                                                              int64_t count4, bool lo_raw) {
+                                                              int64_t count4) {
     asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
-    split_rows_vec4_body<PASSES>(a, hi, lo, count4, blockIdx.x, gridDim.x, lo_raw);
+    split_rows_vec4_body<PASSES>(a, hi, lo, count4, blockIdx.x, gridDim.x);
 }
 
 // Row-major A, general m: one block-row per grid.y step, columns padded to mp.
@@ -75,13 +72,13 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_rows_kernel(const float *__restrict__ a,
                                                          float *__restrict__ hi,
                                                          float *__restrict__ lo, int64_t n,
-                                                         int64_t m, int64_t mp, bool lo_raw) {
+                                                         int64_t m, int64_t mp) {
     asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
         for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < mp;
              c += (int64_t)gridDim.x * blockDim.x) {
             const float x = c < m ? a[r * m + c] : 0.0f;
-            split_store<PASSES>(x, hi, lo, r * mp + c, lo_raw);
+            split_store<PASSES>(x, hi, lo, r * mp + c);
         }
     }
 }
@@ -93,8 +90,7 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__restrict__ b,
                                                               float *__restrict__ hi,
                                                               float *__restrict__ lo, int64_t m,
-                                                              int64_t p, int64_t ldb, int64_t mp,
-                                                              bool lo_raw) {
+                                                              int64_t p, int64_t ldb, int64_t mp) {
     asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     __shared__ float tile[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -109,7 +105,7 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
 #pragma unroll
     for (int i = 0; i < 4; i++) {
         const int64_t j = j0 + ty + 8 * i, k = k0 + tx;
-        if (j < p && k < mp) split_store<PASSES>(tile[tx][ty + 8 * i], hi, lo, j * mp + k, lo_raw);
+        if (j < p && k < mp) split_store<PASSES>(tile[tx][ty + 8 * i], hi, lo, j * mp + k);
     }
 }
 
@@ -119,7 +115,7 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float *__res
 template <int PASSES>
 __device__ __forceinline__ void split_transpose64_body(const float *__restrict__ b, float *__restrict__ hi,
                                                       float *__restrict__ lo, int64_t m, int64_t p, int64_t ldb,
-                                                      int64_t mp, int64_t bx, int64_t by, bool lo_raw,
+                                                      int64_t mp, int64_t bx, int64_t by,
                                                       float (*tile)[65]) {
     const int tid = threadIdx.x;
     const int64_t j0 = bx * 64;  // columns of B = rows of Bt
@@ -151,10 +147,10 @@ __device__ __forceinline__ void split_transpose64_body(const float *__restrict__
         h.w = ptx::to_tf32_rna(x[3]);
         __stcg(reinterpret_cast<float4 *>(hi + j * mp + k), h);
         if constexpr (PASSES == 3) {
-            l.x = lo_part(x[0], h.x, lo_raw);
-            l.y = lo_part(x[1], h.y, lo_raw);
-            l.z = lo_part(x[2], h.z, lo_raw);
-            l.w = lo_part(x[3], h.w, lo_raw);
+            l.x = lo_part(x[0], h.x);
+            l.y = lo_part(x[1], h.y);
+            l.z = lo_part(x[2], h.z);
+            l.w = lo_part(x[3], h.w);
             __stcg(reinterpret_cast<float4 *>(lo + j * mp + k), l);
         }
     }
@@ -164,11 +160,10 @@ template <int PASSES>
 __global__ void __launch_bounds__(256) split_transpose64_kernel(const float *__restrict__ b,
                                                                 float *__restrict__ hi,
                                                                 float *__restrict__ lo, int64_t m,
-                                                                int64_t p, int64_t ldb, int64_t mp,
-                                                                bool lo_raw) {
+                                                                int64_t p, int64_t ldb, int64_t mp) {
     asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     __shared__ float tile[64][65];
-    split_transpose64_body<PASSES>(b, hi, lo, m, p, ldb, mp, blockIdx.x, blockIdx.y, lo_raw, tile);
+    split_transpose64_body<PASSES>(b, hi, lo, m, p, ldb, mp, blockIdx.x, blockIdx.y, tile);
 }
 
 // Both operand splits of one la_gemm in ONE launch (saves a launch and the
@@ -180,14 +175,14 @@ __global__ void __launch_bounds__(256) split_ab_kernel(const float4 *__restrict_
                                                        float4 *__restrict__ alo, int64_t count4, int64_t na,
                                                        const float *__restrict__ b, float *__restrict__ bhi,
                                                        float *__restrict__ blo, int64_t m, int64_t p, int64_t mp,
-                                                       int64_t nbx, bool lo_raw) {
+                                                       int64_t nbx) {
     asm volatile("griddepcontrol.launch_dependents;");  // let the GEMM start its prologue
     __shared__ float tile[64][65];
     if ((int64_t)blockIdx.x < na) {
-        split_rows_vec4_body<PASSES>(a, ahi, alo, count4, blockIdx.x, na, lo_raw);
+        split_rows_vec4_body<PASSES>(a, ahi, alo, count4, blockIdx.x, na);
     } else {
         const int64_t t = (int64_t)blockIdx.x - na;
-        split_transpose64_body<PASSES>(b, bhi, blo, m, p, p, mp, t % nbx, t / nbx, lo_raw, tile);
+        split_transpose64_body<PASSES>(b, bhi, blo, m, p, p, mp, t % nbx, t / nbx, tile);
     }
 }
 
@@ -240,7 +235,7 @@ __device__ __forceinline__ void split_store2(float x0, float x1, float *hi, floa
     const float h0 = ptx::to_tf32_rna(x0), h1 = ptx::to_tf32_rna(x1);
     *reinterpret_cast<float2 *>(hi + off) = make_float2(h0, h1);
     if constexpr (PASSES == 3)
-        *reinterpret_cast<float2 *>(lo + off) = make_float2(lo_part(x0, h0, false), lo_part(x1, h1, false));
+        *reinterpret_cast<float2 *>(lo + off) = make_float2(lo_part(x0, h0), lo_part(x1, h1));
 }
 template <int PASSES>
 __global__ void __launch_bounds__(256) split_complex_a_vec_kernel(const float4 *__restrict__ a, float *__restrict__ hi,

@@ -151,3 +151,57 @@ def test_dgemm_generator_matches_python():
     idx = [0, 7, 99999, 2 ** 33 + 1]
     t = inputs.generate_f64(1, 2 ** 35, 1, col_idx=idx)
     assert t.flatten().tolist() == [inputs.value_int_f64(inputs.SEED, 1, i) for i in idx]
+
+
+# ------------------------------------------------------------------ tolerance scales, exact pins
+def test_complex_abs_scales_exact_integers():
+    """Both outputs of oracle_cabs_scale against exact Python integers (SURVEY
+    8(c): the complex tolerance scales S_r = sum |ar||br| + |ai||bi| and
+    S_i = sum |ar||bi| + |ai||br|).  Integer inputs up to 2^20 in magnitude keep
+    every product (< 2^40) and every sum (< 2^47) exact in binary64, so each
+    scale must equal the integer sum; mixed signs and unequal real/imaginary
+    magnitudes make a swapped pairing (S_i computed with S_r's formula), a
+    dropped |.| or a dropped term differ."""
+    rng = np.random.default_rng(1306)
+    n, m, p = 5, 40, 6
+    ar, ai = rng.integers(-2 ** 20, 2 ** 20, (n, m)), rng.integers(-2 ** 10, 2 ** 10, (n, m))
+    br, bi = rng.integers(-2 ** 20, 2 ** 20, (m, p)), rng.integers(-2 ** 12, 2 ** 12, (m, p))
+    A = (ar + 1j * ai).astype(np.complex64)
+    B = (br + 1j * bi).astype(np.complex64)
+    Sr, Si = oracle.cabs_scale(A, B)
+    for i in range(n):
+        for j in range(p):
+            er = sum(abs(int(ar[i, r])) * abs(int(br[r, j])) + abs(int(ai[i, r])) * abs(int(bi[r, j]))
+                     for r in range(m))
+            ei = sum(abs(int(ar[i, r])) * abs(int(bi[r, j])) + abs(int(ai[i, r])) * abs(int(br[r, j]))
+                     for r in range(m))
+            assert Sr[i, j] == er and Si[i, j] == ei, (i, j)
+    # the two scales are different functions of the inputs here
+    assert not np.array_equal(Sr, Si)
+
+
+def test_double_abs_scale_exact():
+    """oracle_dabs_scale against exact Python integers (integer inputs up to
+    2^24: products < 2^48, m = 30 of them < 2^53, all exact) and,
+    for 2^-52-grid inputs, against the exact rational sum within binary64
+    accumulation error gamma_m * S (Higham) -- an overestimate (e.g. a doubled
+    term) or a missing |.| fails both."""
+    rng = np.random.default_rng(1307)
+    n, m, p = 4, 30, 5
+    A = rng.integers(-2 ** 24, 2 ** 24, (n, m))
+    B = rng.integers(-2 ** 24, 2 ** 24, (m, p))
+    S = oracle.dabs_scale(A.astype(np.float64), B.astype(np.float64))
+    for i in range(n):
+        for j in range(p):
+            assert S[i, j] == sum(abs(int(A[i, r])) * abs(int(B[r, j])) for r in range(m)), (i, j)
+    from fractions import Fraction
+    m = 300
+    Af = inputs.generate_f64(3, m, 0).numpy()
+    Bf = inputs.generate_f64(m, 2, 1).numpy()
+    S = oracle.dabs_scale(Af, Bf)
+    u = 2.0 ** -53
+    g = m * u / (1 - m * u)
+    for i in range(3):
+        for j in range(2):
+            exact = sum(abs(Fraction(Af[i, r])) * abs(Fraction(Bf[r, j])) for r in range(m))
+            assert abs(Fraction(S[i, j]) - exact) <= Fraction(g) * exact
