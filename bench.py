@@ -266,6 +266,35 @@ def run_ours(a, rank, world, local_rank):
     flops = 2.0 * n * m * p
     value = flops / (ms * 1e-3) / 1e12
 
+    # N > 1: the same steps with C assembled on every rank (the
+    # all-gather is reported in its own "with gather" row): ncclAllGather after
+    # the GEMMs, and the fused epilogue storing into every rank's C_full
+    comm = None
+    gather = None
+    if world > 1:
+        nr, crank = la.comm_size()
+        comm = {"ncclCommCount": nr, "rank0_user_rank": crank, "backend": "nccl (library communicator)"}
+        gather = {}
+        for kind in ("nccl", "fused"):
+            Cf = la.gather_buffer(n, p) if kind == "fused" else torch.empty(n, p, device="cuda")
+            for _ in range(max(1, min(a.warmup, 2))):
+                la.gemm_multi(n, m, p, A, B, C, Cf, root=0, ngpu=world, stream=stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(a.steps):
+                la.gemm_multi(n, m, p, A, B, C, Cf, root=0, ngpu=world, stream=stream)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            gt = torch.tensor([g0.elapsed_time(g1) / a.steps], device="cuda")
+            dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+            gms = float(gt.item())
+            gather[kind] = {"ms_per_step": gms, "value": flops / (gms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                            "api": "la_gemm_multi + " + ("ncclAllGather" if kind == "nccl" else
+                                                         "fused epilogue stores into la_gather_alloc C_full")}
+            del Cf
+
     # roofline of the dominant kernel (the GEMM), per launch, this rank
     pk, src = _peaks()
     # The GEMM is the only large kernel and is timed in a region of < 1 s, so the
@@ -390,6 +419,7 @@ def run_ours(a, rank, world, local_rank):
         "pct_tf32_datasheet": 100.0 * passes * flops / (ms * 1e-3) / 1e12 / TF32_DATASHEET_TFLOPS,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": launches, "parity_sample_max_err_units_2^-20": parity,
+        "comm": comm, "gather": gather,
         "paper_context": PAPER_CONTEXT,
     }
     print(json.dumps(line), flush=True)
@@ -408,15 +438,39 @@ PAPER_CONTEXT = [
 ]
 
 
+def _self_launch(a):
+    """--gpus N > 1 outside a torchrun environment: start the N ranks here (one
+    process per GPU through torch.distributed.run, rendezvous on 127.0.0.1) and
+    return the launcher's exit status; rank 0 prints the JSON line."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = _args()
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != a.gpus and "WORLD_SIZE" in os.environ:
-        print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     if a.impl == "reference":
-        return run_reference(a, rank, world)
+        # the oracle runs on the host: rank 0 of a launched job, or this process
+        return run_reference(a, rank, world if launched else a.gpus)
+    if launched and world != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if not launched and a.gpus > 1:
+        return _self_launch(a)
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -192,6 +192,11 @@ LA_API la_status la_get_unique_id(void *out128);
  * Errors: NOT_INITIALIZED, INVALID_VALUE, NCCL. */
 LA_API la_status la_comm_init(const void *uid128, int rank, int ngpu);
 
+/* Ranks in this process's communicator as NCCL reports them (ncclCommCount)
+ * and this process's rank (ncclCommUserRank).  Errors: NOT_INITIALIZED (no
+ * la_comm_init), INVALID_VALUE (NULL), NCCL. */
+LA_API la_status la_comm_size(int *nranks, int *rank);
+
 /* Row-sharded product over the communicator:
  *   rank r owns rows [r*n/g, (r+1)*n/g) of A and C (g = ngpu);
  *   d_A_local : (rows_r x m) row-major fp32;
@@ -200,7 +205,11 @@ LA_API la_status la_comm_init(const void *uid128, int rank, int ngpu);
  *               GEMM on the panels already received;
  *   d_C_local : (rows_r x p) row-major fp32;
  *   d_C_full  : NULL, or n x p: if given, C is all-gathered (ncclAllGather)
- *               into it on every rank (requires n % g == 0).
+ *               into it on every rank (requires n % g == 0).  Reads of d_C_full
+ *               from a previous call must be ordered before this call on
+ *               `stream` (the fused gather of la_gather_alloc writes peers'
+ *               buffers; a cross-rank barrier at the start of the call waits
+ *               for every rank's earlier work on its stream).
  * All ranks pass identical n, m, p, root, ngpu.  Every output element is
  * accumulated in the same order as la_gemm (which never splits K here), so
  * results are bitwise identical to the single-GPU path without split-K.

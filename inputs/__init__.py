@@ -157,3 +157,34 @@ def pair(n: int, m: int, p: int, mode: str = "random", seed: int = SEED, device=
     """(A, B) for the problem n x m by m x p."""
     return (generate(n, m, ID_A, mode, seed, device),
             generate(m, p, ID_B, mode, seed, device))
+
+
+PATTERNS = ("positive", "mixed", "blocks", "ramp", "bias")
+
+
+def structured(A: torch.Tensor, pattern: str, seed: int = SEED) -> torch.Tensor:
+    """Structured variants of a "random"-mode A (n x m) along its K axis (the
+    columns), for accuracy tests beyond symmetric random signs.  Every transform
+    is exact in binary32 (sign flips, powers of two, or -1/4 on the 2^-23 grid),
+    so the exact product stays computable on the 2^-23 grid:
+      positive  |a|                          (same-sign products with |B|)
+      mixed     |a|, negated in the second half of K (one sign change)
+      blocks    |a| times a seeded sign per block of 1024 columns
+      ramp      |a| * 2^floor(10 k / m)      (magnitudes growing along K)
+      bias      a - 1/4                      (mostly negative, with noise)"""
+    m = A.shape[1]
+    k = torch.arange(m, device=A.device)
+    if pattern == "positive":
+        return A.abs()
+    if pattern == "mixed":
+        return torch.where(k >= m // 2, -A.abs(), A.abs())
+    if pattern == "blocks":
+        blk = (k // 1024).to(torch.int64)
+        h = _splitmix64(blk ^ _key(seed, 7))
+        sg = torch.where((h & 1) == 1, -1.0, 1.0).to(A.dtype)
+        return A.abs() * sg[None, :]
+    if pattern == "ramp":
+        return A.abs() * torch.exp2(torch.floor(10.0 * k.to(torch.float64) / m)).to(A.dtype)[None, :]
+    if pattern == "bias":
+        return A - 0.25
+    raise ValueError(f"unknown pattern {pattern!r}; expected one of {PATTERNS}")

@@ -29,7 +29,7 @@ OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3, "nccl_
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
            "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times", "la_cgemm",
-           "la_add", "la_dgemm", "la_gather_alloc", "la_gemm_host_batch")
+           "la_add", "la_dgemm", "la_gather_alloc", "la_gemm_host_batch", "la_comm_size")
 
 
 class LaError(RuntimeError):
@@ -57,6 +57,7 @@ def _load() -> ctypes.CDLL:
         "la_add": ([i64, i64, vp, vp, vp, ctypes.c_int, vp], st),
         "la_get_unique_id": ([vp], st),
         "la_comm_init": ([vp, ctypes.c_int, ctypes.c_int], st),
+        "la_comm_size": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], st),
         "la_gemm_multi": ([i64, i64, i64, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp], st),
         "la_shard_rows": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], st),
         "la_finalize": ([], st),
@@ -302,6 +303,14 @@ def comm_init(uid: bytes, rank: int, ngpu: int) -> None:
     _COMM.update(rank=int(rank), ngpu=int(ngpu))
 
 
+def comm_size():
+    """(nranks, rank) of the library's NCCL communicator (ncclCommCount,
+    ncclCommUserRank)."""
+    a, b = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.la_comm_size(ctypes.byref(a), ctypes.byref(b)), "la_comm_size")
+    return a.value, b.value
+
+
 def bootstrap_unique_id(group=None) -> bytes:
     """Rank 0 of an initialised torch.distributed group creates the NCCL unique
     id (la_get_unique_id); it is broadcast over the group; every rank returns
@@ -356,8 +365,10 @@ def gemm_multi(n, m, p, A_local, B, C_local, C_full=None, root=0, ngpu=1, stream
     _check_dev(C_local, "C_local", shape=None if rows is None else (rows, p))
     if B is not None:
         _check_dev(B, "B", shape=(m, p))
-    if C_full is not None:
-        _check_dev(C_full, "C_full", shape=(n, p))
+    if C_full is not None:   # n x p, or a larger symmetric buffer from gather_buffer (rows >= n)
+        _check_dev(C_full, "C_full")
+        if C_full.shape[1] != p or C_full.shape[0] < n:
+            raise ValueError(f"C_full has shape {tuple(C_full.shape)}, expected ({n}, {p})")
     b = 0 if B is None else B.data_ptr()
     cf = 0 if C_full is None else C_full.data_ptr()
     _check(_lib.la_gemm_multi(n, m, p, A_local.data_ptr(), b, C_local.data_ptr(), cf, int(root), int(ngpu),

@@ -103,6 +103,10 @@ struct GemmArgs {
     const void *gather_win;  // ncclWindow_t (device-resident struct) or nullptr
     int32_t gather_peers;    // LSA team size (<= MAX_GATHER_PEERS)
     int64_t gather_row0, gather_col0, gather_ld;
+    // test hook (one rank emulating gather_peers ranks): 0, or the float
+    // offset between the emulated peers' C_full copies inside this rank's own
+    // window (peer pe's copy at pe * gather_emul_stride)
+    int64_t gather_emul_stride;
 };
 
 constexpr int MAX_GATHER_PEERS = 8;  // one NVLink / NVSwitch domain of 8 GPUs
@@ -378,8 +382,10 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         if (args.gather_win != nullptr)
             for (int pe = 0; pe < args.gather_peers; pe++)
-                gbase[pe] = static_cast<float *>(
-                    ncclGetLsaPointer(reinterpret_cast<ncclWindow_t>(const_cast<void *>(args.gather_win)), 0, pe));
+                gbase[pe] = static_cast<float *>(ncclGetLsaPointer(
+                    reinterpret_cast<ncclWindow_t>(const_cast<void *>(args.gather_win)),
+                    args.gather_emul_stride > 0 ? (size_t)(pe * args.gather_emul_stride) * sizeof(float) : 0,
+                    args.gather_emul_stride > 0 ? 0 : pe));
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_holder, Cfg::TMEM_COLS);
@@ -601,18 +607,30 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     if (e == 0 && lane == 0 && !traced_epi) { trace_stamp(args.trace, 5); traced_epi = true; }
                     ptx::tc_fence_after();
                     const uint32_t taddr = tq + buf * BN;
+                    // two 32-column loads in flight per wait (the drain's latency
+                    // bounds how short a chunk can be without stalling the MMAs)
 #pragma unroll
-                    for (int qq = 0; qq < Cfg::PIECES; qq++) {
+                    for (int qq = 0; qq < Cfg::PIECES; qq += 2) {
                         if (qq < pieces) {
-                            uint32_t v[32];
-                            ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v);
+                            uint32_t v0[32], v1[32];
+                            const bool two = qq + 1 < pieces;
+                            ptx::tmem_ld_32x32b_x32(taddr + qq * 32, v0);
+                            if (two) ptx::tmem_ld_32x32b_x32(taddr + (qq + 1) * 32, v1);
                             ptx::tmem_ld_wait();
                             if (c == 0) {
 #pragma unroll
-                                for (int i = 0; i < 32; i++) acc[qq][i] = __uint_as_float(v[i]);
+                                for (int i = 0; i < 32; i++) acc[qq][i] = __uint_as_float(v0[i]);
+                                if (two) {
+#pragma unroll
+                                    for (int i = 0; i < 32; i++) acc[qq + 1][i] = __uint_as_float(v1[i]);
+                                }
                             } else {
 #pragma unroll
-                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v[i]);
+                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v0[i]);
+                                if (two) {
+#pragma unroll
+                                    for (int i = 0; i < 32; i++) acc[qq + 1][i] += __uint_as_float(v1[i]);
+                                }
                             }
                         }
                     }

@@ -314,6 +314,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.gather_row0 = out.gather_row0;
     args.gather_col0 = out.gather_col0 + j0;
     args.gather_ld = out.gather_ld;
+    args.gather_emul_stride = out.gather_emul_stride;
     args.num_kb = (int32_t)((m + KB - 1) / KB);
     // Promotion only in 3xTF32: plain TF32's 2^-9 bound is 2^11 times looser than
     // the truncation bias of whole-K accumulation (~3 x 2^-20 S at K = 16384).
@@ -330,7 +331,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // on 4096-wide outputs (scripts/promote_cost.py).
     int64_t pk = PASSES == 3 ? g_state.promote_k : 0;
     const int64_t km = out.policy_k > 0 ? out.policy_k : m;
-    if (pk < 0) pk = km <= 64 ? 32 : (km <= 192 ? 64 : (km <= 1024 ? 128 : 256));
+    if (pk < 0) pk = km <= 64 ? 32 : (km <= 192 ? 64 : 128);
     args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + KB - 1) / KB);
     if (args.kc > args.num_kb) args.kc = args.num_kb;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
@@ -378,7 +379,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // Split-K: fewer tiles than half the clusters and a long K -> each tile's K
     // range is cut into S pieces (at least 8 K-blocks each) computed by
     // different clusters; partial tiles go to a workspace and are summed in
-    // order by splitk_reduce_kernel.  Plain real outputs from la_gemm only
+    // order by splitk_reduce_kernel, launched as a programmatic dependent of the
+    // GEMM on the whole GPU.  (An in-kernel fix-up -- the last piece to finish a
+    // region of a tile sums the S slices -- was measured 2.8x slower at C2: one
+    // warp per region reads S x 16 KB latency-bound, ~50 GB/s per SM, on the few
+    // SMs that hold the tiles.)  Plain real outputs from la_gemm only
     // (OutSpec::splitk_ok).  LA_SPLIT_K=0 disables, =S forces S.
     args.ksplit = 1;
     args.kb_per = args.num_kb;
@@ -733,6 +738,7 @@ la_status la_set_option(la_option option, int64_t value) {
             if (value < 0 || value > 64) return fail(LA_ERR_INVALID_VALUE, "nccl_sms must be in [0, 64]");
             g_state.nccl_sms = value;
             return LA_OK;
+
     }
     return fail(LA_ERR_INVALID_VALUE, "unknown option %d", (int)option);
 }

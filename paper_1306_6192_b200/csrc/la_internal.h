@@ -18,13 +18,12 @@ struct State {
     uint64_t generation = 0;  // bumped by every la_init: per-device setup cached in statics is redone
     cudaMemPool_t pool = nullptr;
     la_mode mode = LA_MODE_3XTF32;
-    // Accumulator promotion interval in K elements (0 = whole K in TMEM).
-    // Default 256: the tcgen05 kind::tf32 accumulator truncates (probe in
-    // tests/test_probe.py); promotion every 256 keeps 3xTF32 at ~0.06 x 2^-20 S.
+    // Accumulator promotion interval in K elements (0 = whole K in TMEM): the
+    // tcgen05 kind::tf32 accumulator truncates (probes in tests/test_probe.py).
     int64_t promote_k = -1;  // -1: automatic by K (launch_gemm)
     int64_t max_sms = 0;
     int64_t panels = 4;
-    int64_t nccl_sms = 8;  // SMs left to NCCL (ncclConfig_t.maxCTAs) while B panels are in flight
+    int64_t nccl_sms = 8;    // SMs left to NCCL (ncclConfig_t.maxCTAs) while B panels are in flight
     int last_launches = 0;
     void *staging = nullptr;  // la_gemm_host device staging
     size_t staging_bytes = 0;
@@ -57,6 +56,9 @@ la_status fail(la_status s, const char *fmt, ...);
 //   LA_HOST_PANELS=q       host transfer panels                (tests/test_parity.py)
 //   LA_DGEMM_CPASYNC=1     cp.async DGEMM instead of TMA       (tests/test_parity_ext.py)
 //   LA_TEST_GATHER_ROW0=r  fused-gather destination row, 1 rank (tests/test_multi.py)
+//   LA_TEST_GATHER_PEERS=g, LA_TEST_GATHER_STRIDE=s  one rank emulating g ranks'
+//                          C_full copies at float offsets 0, s, 2s.. of its own
+//                          window (tests/test_multi.py)
 // Experiment knobs (LA_SPLIT_T32, LA_GROUP_M, LA_WAVE_SYNC, LA_HOST_TAIL_SPLIT,
 // LA_HOST_TRACE, LA_DIAG_CLUSTERS, LA_DIAG_TRACE, LA_DEBUG_KERNEL) are read only
 // in the diagnostics build (LA_BUILD_DIAGNOSTICS=1); elsewhere diag_knob
@@ -92,6 +94,7 @@ struct OutSpec {
     const void *gather_win = nullptr;
     int gather_peers = 0;
     int64_t gather_row0 = 0, gather_col0 = 0, gather_ld = 0;
+    int64_t gather_emul_stride = 0;  // test hook: emulated peers inside one window (GemmArgs)
     // la_gemm may split K across clusters when there are few output tiles (the
     // multi-GPU path never does, so its result stays bitwise equal to la_gemm
     // without split-K)

@@ -138,6 +138,15 @@ la_status la_comm_init(const void *uid128, int rank, int ngpu) {
     return LA_OK;
 }
 
+la_status la_comm_size(int *nranks, int *rank) {
+    std::lock_guard<std::recursive_mutex> lk(g_mutex);
+    if (!nranks || !rank) return fail(LA_ERR_INVALID_VALUE, "NULL output pointer");
+    if (!g_comm.comm) return fail(LA_ERR_NOT_INITIALIZED, "la_comm_init has not been called");
+    LA_NCCL(ncclCommCount(g_comm.comm, nranks));
+    LA_NCCL(ncclCommUserRank(g_comm.comm, rank));
+    return LA_OK;
+}
+
 la_status la_gather_alloc(int64_t bytes, void **d_out) {
     std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
@@ -234,12 +243,21 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
         out.gather_peers = g_comm.lsa_size;
         out.gather_row0 = row0;
         out.gather_ld = p;
+        // test hooks (one rank): a non-zero destination row, and g emulated
+        // peers whose C_full copies sit at offsets 0, s, 2s.. of this window
         const int64_t hook_row0 = ngpu == 1 ? test_hook("LA_TEST_GATHER_ROW0", -1) : -1;
-        if (hook_row0 >= 0) {  // test hook: exercise a non-zero destination row with one rank
-            out.gather_row0 = hook_row0;
-            if ((size_t)((out.gather_row0 + rows) * p) * sizeof(float) > g_comm.gather_bytes)
-                return fail(LA_ERR_INVALID_VALUE, "LA_TEST_GATHER_ROW0 past the gather buffer");
+        const int64_t hook_peers = ngpu == 1 ? test_hook("LA_TEST_GATHER_PEERS", 1) : 1;
+        const int64_t hook_stride = ngpu == 1 ? test_hook("LA_TEST_GATHER_STRIDE", 0) : 0;
+        if (hook_row0 >= 0) out.gather_row0 = hook_row0;
+        if (hook_peers > 1) {
+            if (hook_peers > MAX_GATHER_PEERS || hook_stride < (out.gather_row0 + rows) * p)
+                return fail(LA_ERR_INVALID_VALUE, "bad LA_TEST_GATHER_PEERS / LA_TEST_GATHER_STRIDE");
+            out.gather_peers = (int)hook_peers;
+            out.gather_emul_stride = hook_stride;
         }
+        const int64_t span = (out.gather_peers - 1) * out.gather_emul_stride + (out.gather_row0 + rows) * p;
+        if ((size_t)span * sizeof(float) > g_comm.gather_bytes)
+            return fail(LA_ERR_INVALID_VALUE, "fused gather test hooks reach past the gather buffer");
     }
     // comm stream starts after everything already queued on the caller's stream
     LA_CK(cudaEventRecord(g_comm.start, st));

@@ -18,7 +18,7 @@ def _declared():
 def test_header_and_binding_agree():
     import paper_1306_6192_b200 as la
     declared = _declared()
-    assert len(declared) == 20
+    assert len(declared) == 21
     assert sorted(declared) == sorted(la.EXPORTS)
 
 
@@ -64,6 +64,10 @@ def test_not_initialized_and_argument_errors():
     assert lib.la_set_option(la.OPTIONS["panels"], 0) == la.LA_ERR_INVALID_VALUE
     # no device in this container: la_init reports it instead of crashing
     assert lib.la_init(0) in (la.LA_ERR_INVALID_VALUE, la.LA_ERR_CUDA)
+    import ctypes
+    a, b = ctypes.c_int(), ctypes.c_int()
+    assert lib.la_comm_size(ctypes.byref(a), ctypes.byref(b)) == la.LA_ERR_NOT_INITIALIZED
+    assert lib.la_comm_size(None, None) == la.LA_ERR_INVALID_VALUE
     assert la.finalize() is None
 
 
@@ -77,6 +81,9 @@ def test_options_roundtrip():
     assert la.get_option("promote_k") == -1
     with pytest.raises(la.LaError):
         la.set_option("promote_k", -2)
+    assert la.get_option("nccl_sms") == 8
+    with pytest.raises(la.LaError):
+        la.set_option("nccl_sms", -1)
 
 
 def test_shard_rows_partition():

@@ -39,3 +39,32 @@ def test_committed_gpu_line_has_every_key():
     assert e2e["h2d_bytes_per_step"] == 2 * 4 * 16384 ** 2 and e2e["d2h_bytes_per_step"] == 4 * 16384 ** 2
     assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert line["gpu_launches"] > 0
+
+
+def test_multi_gpu_request_is_never_silently_single():
+    """`bench.py --gpus N` without a torchrun environment launches N ranks
+    itself; with fewer visible GPUs than N it must fail loudly instead of
+    timing one GPU under an N-GPU line."""
+    import torch
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    if torch.cuda.device_count() >= 2:
+        import pytest
+        pytest.skip("enough GPUs: the launch itself is exercised by the driver's scaling run")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0
+    assert "--gpus 2" in r.stderr
+    # a launched job whose WORLD_SIZE disagrees with --gpus is refused too
+    env.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr
+
+
+def test_reference_arm_reports_requested_gpus():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "4", "--steps", "1",
+                        "--warmup", "0", "--cpu-seconds", "1", "--n", "1024"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1])["n_gpus"] == 4

@@ -173,3 +173,42 @@ def test_fused_gather_row_offset(la1, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(Cf[7:7 + n], ref)
     assert torch.all(Cf[:7] == -7.0) and torch.all(Cf[7 + n:] == -7.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g,kind", [(2, "integer"), (3, "stress"), (4, "integer"), (8, "stress")])
+def test_fused_gather_emulated_ranks_vs_oracle(la1, g, kind, monkeypatch):
+    """One GPU emulating g ranks of the fused GEMM -> all-gather (SURVEY 8(f)
+    NEXT #1): every emulated rank r runs la_gemm_multi on its own rows of A
+    (la_shard_rows) with the test hooks LA_TEST_GATHER_ROW0 = its first row and
+    LA_TEST_GATHER_PEERS = g, so its epilogue stores its rows into g C_full
+    copies (consecutive regions of one symmetric window, standing in for the g
+    ranks' buffers).  The launches do not wait on one another.  After the g
+    calls every copy must hold the whole product: the oracle exactly on
+    integer inputs, within 2^-20 * sum|a||b| on stress inputs."""
+    import oracle
+    la = la1
+    la.set_option("panels", 2)
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    n, m, p = 97 * g + 31, 300, 520
+    A, B = inputs.pair(n, m, p, kind, device="cuda")
+    Cf = la.gather_buffer(g * n, p)
+    Cf.fill_(-3.0)
+    monkeypatch.setenv("LA_TEST_GATHER_PEERS", str(g))
+    monkeypatch.setenv("LA_TEST_GATHER_STRIDE", str(n * p))
+    for r in range(g):
+        row0, rows = la.shard_rows(n, r, g)
+        monkeypatch.setenv("LA_TEST_GATHER_ROW0", str(row0))
+        Cl = torch.empty(rows, p, device="cuda")
+        la.gemm_multi(rows, m, p, A[row0:row0 + rows].contiguous(), B, Cl, Cf, root=0, ngpu=1)
+    torch.cuda.synchronize()
+    An, Bn = A.cpu().numpy(), B.cpu().numpy()
+    ref = oracle.gemm(An, Bn, threads=8)
+    S = oracle.abs_scale(An, Bn)
+    copies = Cf.cpu().numpy().reshape(g, n, p)
+    for pe in range(g):
+        if kind == "integer":
+            assert np.array_equal(copies[pe], ref), pe
+        else:
+            assert float((np.abs(copies[pe].astype(np.float64) - ref) / S).max()) <= 2.0 ** -20, pe
+    assert np.array_equal(copies[0], copies[g - 1])

@@ -288,8 +288,9 @@ def test_n65536_indexing_sampled(la):
 @pytest.mark.parametrize("n,m,p", [(512, 16384, 512), (1000, 2000, 1500), (64, 50000, 96), (300, 4096, 257)])
 def test_split_k_parity(la, n, m, p, monkeypatch):
     """Few output tiles and a long K take the split-K path (partials reduced in
-    order): integer inputs exact, stress inputs within 2^-20, run-to-run bitwise,
-    and the forced split factors agree with the unsplit result within bound."""
+    piece order by a second kernel):
+    integer inputs exact, stress inputs within 2^-20, run-to-run bitwise, and
+    the forced split factors agree with the unsplit result within bound."""
     A, B = inputs.pair(n, m, p, "integer", device="cuda")
     rows = sorted({0, n // 3, n - 1})
     C = la.gemm(A, B)

@@ -82,6 +82,25 @@ def test_probe_negative(la):
     assert lab in ("RN/RD", "RZ/RU")
 
 
+# Accumulator against products: how a product sum below the accumulator's ulp
+# is added (two MMAs: the first sets D, the second adds the small sum).
+#   exact+RZ      : D + sum formed exactly, then rounded toward zero
+#   sum-truncated : the sum aligned to D's ulp and truncated toward zero (its
+#                   error has the sign of -sum, whatever D's sign), then added
+#   floor         : two's-complement truncation (toward -inf) of the sum
+def test_probe_accumulator_opposite_sign(la):
+    d = 1.5 * 2.0 ** -24
+    c1 = _row_dot(la, [-1.0] + [0.0] * 7 + [d] + [0.0] * 7)
+    lab1 = _record("neg_acc_plus_small", c1, {"exact+RZ": -(1 - U), "sum-truncated/floor": -1.0})
+    c2 = _row_dot(la, [1.0] + [0.0] * 7 + [-d] + [0.0] * 7)
+    lab2 = _record("pos_acc_minus_small", c2, {"exact+RZ/floor": 1 - U, "sum-truncated": 1.0})
+    c3 = _row_dot(la, [-1.0] + [0.0] * 7 + [-d] + [0.0] * 7)
+    lab3 = _record("neg_acc_minus_small", c3, {"exact+RZ/sum-truncated": -1.0, "floor": -(1 + U)})
+    c4 = _row_dot(la, [1.0] + [0.0] * 7 + [0.75 * U, 0.75 * U] + [0.0] * 6)
+    lab4 = _record("two_sub_half_ulp_products", c4, {"sum-then-truncate": 1 + U, "per-product": 1.0})
+    assert "other" not in (lab1, lab2, lab3, lab4), (c1, c2, c3, c4)
+
+
 def test_probe_long_k_accuracy(la, monkeypatch):
     """3xTF32 at K = 16384 on 24-bit inputs: max error / (2^-20 S) without
     promotion and with promotion every 1024 / 256.  Split-K is off, so each
