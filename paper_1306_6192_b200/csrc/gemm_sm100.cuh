@@ -49,9 +49,8 @@ namespace la {
 constexpr int BK = 32;            // default K per stage: 32 fp32 = one 128-byte swizzle row
                                   // (KB = 16: 64-byte rows, SWIZZLE_64B, twice the stages)
 constexpr int ROWS_PER_CTA = 128; // UMMA M per CTA
-constexpr int NUM_CTRL_WARPS = 4; // warp0 TMA, warp1 MMA, warp2 TMEM alloc (+ FUSE: warps 2, 3 split)
+constexpr int NUM_CTRL_WARPS = 4; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 idle
 constexpr int NUM_EPI_WARPS = 8;  // two per TMEM lane quarter (column halves)
-constexpr int NUM_CONV_WARPS = 2; // FUSE: warps 2 and 3 split the staged fp32 tiles in smem
 constexpr int NUM_THREADS = 32 * (NUM_CTRL_WARPS + NUM_EPI_WARPS);
 // setmaxnreg budgets.  A CTA's register pool is what it was launched with:
 // __launch_bounds__(384, 1) gives 168 registers x 384 threads = 64512; the
@@ -59,9 +58,7 @@ constexpr int NUM_THREADS = 32 * (NUM_CTRL_WARPS + NUM_EPI_WARPS);
 // to EPI_REGS, and the sum must stay inside that pool or setmaxnreg.inc
 // blocks forever.  (ptxas still allocates every region within the launch
 // bound's 168, so the promotion loop's 128 running sums + two 32-column loads
-// spill a few registers; a 512-thread CTA -- 128 registers -- would spill the
-// running sums themselves, which is why the fused split's converters are the
-// otherwise idle control warps and not an extra warpgroup.)
+// spill a few registers.)
 constexpr int LAUNCH_REGS = 168;
 constexpr int CTRL_REGS = 56;
 constexpr int EPI_REGS = 216;
@@ -183,9 +180,8 @@ __device__ __forceinline__ void wave_barrier(int32_t *ctr, int target, int32_t *
     }
 }
 
-template <int CG, int BN, int STAGES, int PASSES, int KB = BK, bool FUSE = false>
+template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 struct GemmCfg {
-    static constexpr int THREADS = NUM_THREADS;
     static constexpr int TILE_M = CG * ROWS_PER_CTA;        // rows of C per tile
     static constexpr int B_ROWS = BN / CG;                  // rows of B^T staged per CTA
     static constexpr int NOPS = PASSES == 3 ? 2 : 1;        // hi (+ lo) tiles per operand
@@ -208,14 +204,6 @@ struct GemmCfg {
     static_assert(BN % 64 == 0 && BN <= 256, "UMMA N: multiple of 16 (32 per epilogue piece), <= 256");
     static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM alloc is a power of 2");
     static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB of shared memory per CTA");
-    // FUSE: A is staged K-major straight from row-major A; B arrives N-major
-    // from row-major B in boxes of 32 columns x KB rows (128-byte swizzle), and
-    // each 4 KB box occupies exactly the bytes of the 32 K-major rows it becomes
-    // (rows bx*32.. of the B^T tile), so the converter transposes it in place.
-    static constexpr int B_BOX_N = 32;
-    static constexpr int B_BOXES = B_ROWS / B_BOX_N;
-    static constexpr int B_BOX_BYTES = B_BOX_N * KB * 4;  // 4 KB at KB = 32
-    static_assert(!FUSE || KB == 32, "fused split: one 128-byte swizzle atom of K per stage");
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int &tm, int &tn) {
@@ -226,19 +214,6 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
     const int r = t - g * per_group;
     tm = first + r % gsz;
     tn = r / gsz;
-}
-
-// The 3xTF32 split of four fp32 bit patterns (split.cuh): hi = tf32_rna(x),
-// lo = tf32_rna(x - hi).
-__device__ __forceinline__ uint4 split_hi4(uint4 x) {
-    return make_uint4(ptx::tf32_rna_bits(x.x), ptx::tf32_rna_bits(x.y), ptx::tf32_rna_bits(x.z),
-                      ptx::tf32_rna_bits(x.w));
-}
-__device__ __forceinline__ uint32_t split_lo1(uint32_t x, uint32_t h) {
-    return ptx::tf32_rna_bits(__float_as_uint(__uint_as_float(x) - __uint_as_float(h)));
-}
-__device__ __forceinline__ uint4 split_lo4(uint4 x, uint4 h) {
-    return make_uint4(split_lo1(x.x, h.x), split_lo1(x.y, h.y), split_lo1(x.z, h.z), split_lo1(x.w, h.w));
 }
 
 // Work item w -> tile (tm, tn), part (-1 = whole tile, 0/1 = column half) and
@@ -334,12 +309,12 @@ __device__ __forceinline__ void store_piece(const GemmArgs &args, float *tbuf, u
     __syncwarp();
 }
 
-template <int CG, int BN, int STAGES, int PASSES, int KB = BK, bool FUSE = false>
+template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tf32_sm100_kernel(const __grid_constant__ CUtensorMap tm_a_hi, const __grid_constant__ CUtensorMap tm_a_lo,
                            const __grid_constant__ CUtensorMap tm_b_hi, const __grid_constant__ CUtensorMap tm_b_lo,
                            const __grid_constant__ CUtensorMap tm_c, const GemmArgs args) {
-    using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB, FUSE>;
+    using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // stage s: [A_hi | A_lo | B_hi | B_lo]   (identical offsets in both CTAs of a pair)
@@ -354,10 +329,6 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
     float **gbase = reinterpret_cast<float **>(reinterpret_cast<uint8_t *>(full) + 320);  // [MAX_GATHER_PEERS]
-    // FUSE: full[s] = this CTA's fp32 tiles landed (own producer), cfull[s] (leader)
-    // = both CTAs' tiles split into hi / lo and visible to the tensor core
-    uint64_t *cfull = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(full) + 448);  // [STAGES]
-    static_assert(448 + 8 * STAGES <= Cfg::BAR_BYTES, "barrier area");
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -379,10 +350,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < STAGES; s++) {
-            ptx::mbar_init(&full[s], 1);   // leader producer's arrive.expect_tx (+ tx bytes of both CTAs);
-                                           // FUSE: this CTA's producer (+ this CTA's tx bytes)
+            ptx::mbar_init(&full[s], 1);   // leader producer's arrive.expect_tx (+ tx bytes of both CTAs)
             ptx::mbar_init(&empty[s], 1);  // one tcgen05.commit (multicast to both CTAs)
-            if constexpr (FUSE) ptx::mbar_init(&cfull[s], CG * NUM_CONV_WARPS);  // converter warps of the pair
         }
         for (int b = 0; b < 2; b++) {
             ptx::mbar_init(&tfull[b], 1);                      // one tcgen05.commit
@@ -440,21 +409,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     __syncwarp();
                 }
                 ptx::mbar_wait(&empty[s], ph ^ 1);
-                if constexpr (FUSE) {
-                    // fp32 tiles straight from A (K-major box, into the A_hi
-                    // slot) and B (N-major boxes of 32 columns, into the B_lo
-                    // slot, or B_hi with one pass); the converter warps split
-                    // them in place (and transpose B)
-                    if (lane == 0) {
-                        const int32_t k0 = kb * KB;
-                        ptx::mbar_arrive_expect_tx(&full[s], Cfg::A_TILE + Cfg::B_TILE);
-                        ptx::tma_load_2d(a_tile(s, 0), &tm_a_hi, &full[s], k0, m0, pol);
-#pragma unroll
-                        for (int bx = 0; bx < Cfg::B_BOXES; bx++)
-                            ptx::tma_load_2d(b_tile(s, Cfg::NOPS - 1) + bx * Cfg::B_BOX_BYTES, &tm_b_hi, &full[s],
-                                             n0 + bx * Cfg::B_BOX_N, k0, pol);
-                    }
-                } else if (lane == 0 && (args.debug & 1)) {
+                if (lane == 0 && (args.debug & 1)) {
                     if (rank == 0) ptx::mbar_arrive(&full[s]);
                 } else if (lane == 0) {
                     const int32_t k0 = kb * KB;
@@ -498,12 +453,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     else ptx::mbar_wait(&tempty[buf], aph ^ 1);
                     ptx::tc_fence_after();
                 }
-                if constexpr (FUSE) {
-                    if constexpr (CG == 2) ptx::mbar_wait_cluster(&cfull[s], ph);
-                    else ptx::mbar_wait(&cfull[s], ph);
-                } else {
-                    ptx::mbar_wait(&full[s], ph);
-                }
+                ptx::mbar_wait(&full[s], ph);
                 if (lane == 0 && kb == kb0 && !traced_mma) { trace_stamp(args.trace, 3); traced_mma = true; }
                 ptx::tc_fence_after();
                 {
@@ -545,74 +495,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
         }
         if (lane == 0) trace_stamp(args.trace, 4);
-    } else if (FUSE && (warp == 2 || warp == 3)) {
-        // ======================= converter (both CTAs, FUSE) =======================
-        // The operand split of split.cuh done on the staged tiles, by the two
-        // otherwise idle control warps (2: TMEM allocator, 3):
-        //   A: every fp32 x of the K-major tile becomes hi = tf32_rna(x) in place
-        //      and lo = tf32_rna(x - hi) at the same offset of the lo slot
-        //      (elementwise on 16-byte chunks, so the swizzle is the same);
-        //   B: each N-major 4 KB box (32 columns x 32 K rows) is read whole into
-        //      registers (lane = column: row k's 128-byte line holds column c in
-        //      16-byte chunk (c/4) ^ (k%8)), then written back transposed as the
-        //      32 K-major rows of B^T it occupies (row r: chunk j at j ^ (r%8)),
-        //      hi into the hi slot, lo into the lo slot in place.
-        // Generic-proxy writes are fenced for the tensor core (async proxy)
-        // before the arrive on the leader's cfull[s].
-        const uint32_t cw = warp - 2;  // 0, 1
-        constexpr int A4 = Cfg::A_TILE / 16, CT = 32 * NUM_CONV_WARPS;
-        static_assert(A4 % CT == 0 && Cfg::B_BOXES % NUM_CONV_WARPS == 0, "converter work split");
-        int s = 0;
-        uint32_t ph = 0;
-        for (int t = cluster_id; t < num_items; t += num_clusters) {
-            int tm_, tn_, part_, kb0, kb1, ks_;
-            decode_item(t, args, tm_, tn_, part_, kb0, kb1, ks_);
-            for (int kb = kb0; kb < kb1; kb++) {
-                ptx::mbar_wait(&full[s], ph);
-                if (!(args.debug & 4)) {
-                    const uint32_t ah = ptx::smem_u32(a_tile(s, 0)), al = ptx::smem_u32(a_tile(s, Cfg::NOPS - 1));
-#pragma unroll
-                    for (int it = 0; it < A4 / CT; it += 4) {
-                        uint4 x[4];
-#pragma unroll
-                        for (int u = 0; u < 4; u++) x[u] = ptx::lds128(ah + (((it + u) * CT + cw * 32 + lane) << 4));
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const uint32_t o = ((it + u) * CT + cw * 32 + lane) << 4;
-                            const uint4 h = split_hi4(x[u]);
-                            ptx::sts128(ah + o, h);
-                            if constexpr (PASSES == 3) ptx::sts128(al + o, split_lo4(x[u], h));
-                        }
-                    }
-                }
-                if (!(args.debug & 8)) {
-#pragma unroll 1
-                    for (int bx = cw; bx < Cfg::B_BOXES; bx += NUM_CONV_WARPS) {
-                        const uint32_t raw = ptx::smem_u32(b_tile(s, Cfg::NOPS - 1)) + bx * Cfg::B_BOX_BYTES;
-                        const uint32_t hib = ptx::smem_u32(b_tile(s, 0)) + bx * Cfg::B_BOX_BYTES;
-                        const uint32_t rd = raw + ((lane & 3) << 2), chunk = lane >> 2;
-                        uint32_t v[32];
-#pragma unroll
-                        for (int k = 0; k < 32; k++) v[k] = ptx::lds32(rd + k * 128 + ((chunk ^ (k & 7)) << 4));
-                        __syncwarp();
-#pragma unroll
-                        for (int c = 0; c < 8; c++) {
-                            const uint32_t off = lane * 128 + ((c ^ (lane & 7)) << 4);
-                            const uint4 x = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-                            const uint4 h = split_hi4(x);
-                            ptx::sts128(hib + off, h);
-                            if constexpr (PASSES == 3) ptx::sts128(raw + off, split_lo4(x, h));
-                        }
-                    }
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_cta0<CG>(&cfull[s]);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
-            }
-        }
     }
-    } else if (warp < NUM_CTRL_WARPS + NUM_EPI_WARPS) {
+    } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
         // ======================= epilogue (both CTAs) =======================
         const uint32_t e = warp - NUM_CTRL_WARPS;

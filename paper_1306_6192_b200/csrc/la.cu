@@ -80,11 +80,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
 // 2-D fp32 tensor map over a rows x cols row-major buffer (cols % 4 == 0),
 // box = box_rows x 32 columns, 128-byte swizzle, OOB elements read as zero.
 static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols,
-                           int box_rows, int box_k = BK, int64_t ld = 0) {
+                           int box_rows, int box_k = BK) {
     auto enc = get_encoder();
     if (!enc) return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld > 0 ? ld : cols) * sizeof(float)};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
     cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)box_rows};  // box_rows <= 256
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides,
@@ -285,29 +285,19 @@ static int splitk_factor(int64_t tiles, int64_t slots, int num_kb) {
     return (num_kb + per - 1) / per;
 }
 
-template <int CG, int BN, int STAGES, int PASSES, int KB = BK, bool FUSE = false>
+template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
 static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands &ops, float *C,
                              int64_t ldc, int max_sms, cudaStream_t st, int *launches, const OutSpec &out) {
-    using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB, FUSE>;
+    using Cfg = GemmCfg<CG, BN, STAGES, PASSES, KB>;
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     la_status s;
-    if (FUSE) {
-        // fp32 operands read in place: A K-major boxes of 32 x 128, B N-major
-        // boxes of 32 columns x 32 rows (K) at column j0 of the caller's B
-        if ((s = make_tmap(&ta_hi, ops.raw_a, n, m, ROWS_PER_CTA, BK)) != LA_OK) return s;
-        if ((s = make_tmap(&tb_hi, ops.raw_b + j0, m, pc, BK, Cfg::B_BOX_N, ops.ldb)) != LA_OK) return s;
-        ta_lo = ta_hi;
-        tb_lo = tb_hi;
-    } else if (PASSES == 3) {
-        const float *bh = ops.b_hi + j0 * ops.mp, *bl = ops.b_lo + j0 * ops.mp;
-        if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA, Cfg::ATOM_K)) != LA_OK) return s;
-        if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS, Cfg::ATOM_K)) != LA_OK) return s;
+    const float *bh = ops.b_hi + j0 * ops.mp, *bl = ops.b_lo + j0 * ops.mp;
+    if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA, Cfg::ATOM_K)) != LA_OK) return s;
+    if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS, Cfg::ATOM_K)) != LA_OK) return s;
+    if (PASSES == 3) {
         if ((s = make_tmap(&ta_lo, ops.a_lo, n, ops.mp, ROWS_PER_CTA, Cfg::ATOM_K)) != LA_OK) return s;
         if ((s = make_tmap(&tb_lo, bl, pc, ops.mp, Cfg::B_ROWS, Cfg::ATOM_K)) != LA_OK) return s;
     } else {
-        const float *bh = ops.b_hi + j0 * ops.mp;
-        if ((s = make_tmap(&ta_hi, ops.a_hi, n, ops.mp, ROWS_PER_CTA, Cfg::ATOM_K)) != LA_OK) return s;
-        if ((s = make_tmap(&tb_hi, bh, pc, ops.mp, Cfg::B_ROWS, Cfg::ATOM_K)) != LA_OK) return s;
         ta_lo = ta_hi;
         tb_lo = tb_hi;
     }
@@ -349,7 +339,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     args.group_m = (int32_t)std::max<int64_t>(1, diag_knob("LA_GROUP_M", 8));
     const int64_t tiles = (int64_t)args.tiles_m * args.tiles_n;
 
-    auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES, KB, FUSE>;
+    auto kern = gemm_tf32_sm100_kernel<CG, BN, STAGES, PASSES, KB>;
     // per-device setup, redone after la_finalize + la_init (possibly another device)
     static int max_clusters = 0;
     static uint64_t setup_gen = 0;
@@ -358,7 +348,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)", __FILE__, __LINE__);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(CG * g_state.sms / CG);
-        cfg.blockDim = dim3(Cfg::THREADS);
+        cfg.blockDim = dim3(NUM_THREADS);
         cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
         cudaLaunchAttribute attr;
         attr.id = cudaLaunchAttributeClusterDimension;
@@ -462,7 +452,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
         args.trace = trace_buf;
     }
 #else
-    args.debug = (int32_t)test_hook("LA_TMP_DEBUG", 0);
+    args.debug = 0;
 #endif
     args.wave_sync = nullptr;
     args.wave_slots = 0;
@@ -501,7 +491,7 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // reading their output
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(clusters * CG));
-    lc.blockDim = dim3(Cfg::THREADS);
+    lc.blockDim = dim3(NUM_THREADS);
     lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
     lc.stream = st;
     cudaLaunchAttribute la_attr[1];
@@ -607,16 +597,6 @@ la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands 
     const int cg = choose_cta_group(n, pc, num_kb, splitk_ok);
     // (KB = 16 with a 6-stage ring was measured slower and costlier: 202 vs 244
     // TFLOP/s and 42.9 vs 35.3 J per n = 16384 GEMM -- not dispatched.)
-    if (ops.fused) {
-        if (ops.passes == 3) {
-            if (cg == 2)
-                return launch_gemm<2, 256, kStages3, 3, BK, true>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
-            return launch_gemm<1, 128, kStages3, 3, BK, true>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
-        }
-        if (cg == 2)
-            return launch_gemm<2, 256, kStages1, 1, BK, true>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
-        return launch_gemm<1, 128, kStages1, 1, BK, true>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
-    }
     if (ops.passes == 3) {
         if (cg == 2) return launch_gemm<2, 256, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
         return launch_gemm<1, 128, kStages3, 3>(n, m, j0, pc, ops, C, ldc, max_sms, st, launches, out);
@@ -654,30 +634,10 @@ la_status validate_gemm(int64_t n, int64_t m, int64_t p, const float *A, const f
     return LA_OK;
 }
 
-// The fused split (Operands::fused) applies when TMA can read A and B in
-// place: 16-byte row strides and base addresses.  LA_FUSED_SPLIT=0 selects the
-// separate split pass (test hook: the two paths must agree bitwise).
-bool fused_split_ok(int64_t m, int64_t ldb, const float *A, const float *B) {
-    if (test_hook("LA_FUSED_SPLIT", 0) == 0) return false;  // experiment, off by default
-    return m % 4 == 0 && ldb % 4 == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
-}
-
 // C (n x p, row stride ldc) = A (n x m) . B (m x p), one GPU.
 static la_status gemm_impl(int64_t n, int64_t m, int64_t p, const float *A, const float *B, float *C, int64_t ldc,
                            cudaStream_t st, int *launches) {
     const int passes = g_state.mode == LA_MODE_TF32 ? 1 : 3;
-    OutSpec out;
-    out.splitk_ok = true;
-    if (fused_split_ok(m, p, A, B)) {
-        Operands ops;
-        ops.fused = true;
-        ops.raw_a = A;
-        ops.raw_b = B;
-        ops.ldb = p;
-        ops.mp = m;
-        ops.passes = passes;
-        return gemm_run(n, m, 0, p, ops, C, ldc, (int)g_state.max_sms, st, launches, out);
-    }
     const size_t bytes = operands_bytes(n, m, p, passes);
     void *ws = nullptr;
     cudaError_t e = cudaMallocFromPoolAsync(&ws, bytes, g_state.pool, st);
@@ -691,6 +651,8 @@ static la_status gemm_impl(int64_t n, int64_t m, int64_t p, const float *A, cons
         s = split_a(n, m, A, ops, st, launches);
         if (s == LA_OK) s = split_b(m, 0, p, B, p, ops, st, launches);
     }
+    OutSpec out;
+    out.splitk_ok = true;
     if (s == LA_OK) s = gemm_run(n, m, 0, p, ops, C, ldc, (int)g_state.max_sms, st, launches, out);
     e = cudaFreeAsync(ws, st);
     if (s == LA_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync", __FILE__, __LINE__);

@@ -75,14 +75,6 @@ struct Operands {
     float *b_hi = nullptr, *b_lo = nullptr;  // p x mp
     int64_t mp = 0;
     int passes = 3;
-    // Fused split (the GEMM's converter warps split the staged fp32 tiles in
-    // shared memory; no K1 pass, no workspace): the caller's A (n x m, row
-    // stride m) and B (m x p block at column j0 of a row-major matrix with row
-    // stride ldb) are read directly.  Needs m % 4 == 0, ldb % 4 == 0 and
-    // 16-byte aligned A, B (TMA strides and addresses).
-    bool fused = false;
-    const float *raw_a = nullptr, *raw_b = nullptr;
-    int64_t ldb = 0;
 };
 
 inline int64_t pad_k(int64_t m) { return (m + 3) / 4 * 4; }
@@ -120,6 +112,5 @@ la_status gemm_run(int64_t n, int64_t m, int64_t j0, int64_t pc, const Operands 
                    int max_sms, cudaStream_t st, int *launches, OutSpec out = OutSpec());
 
 la_status comm_destroy();
-bool fused_split_ok(int64_t m, int64_t ldb, const float *A, const float *B);
 
 }  // namespace la

@@ -331,26 +331,9 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
 // low bits cleared; a carry out of the mantissa bumps the exponent.  For every
 // finite input this is exactly cvt.rna.tf32.f32 (which spends two more
 // instructions keeping NaN payloads; non-finite inputs are out of contract,
-// SURVEY 8(c) C16).  Two integer ops, so the fused split's converter warps can
-// keep up with the tensor pipe.
+// SURVEY 8(c) C16).
 __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x) { return (x + 0x1000u) & 0xFFFFE000u; }
 __device__ __forceinline__ float to_tf32_rna(float x) { return __uint_as_float(tf32_rna_bits(__float_as_uint(x))); }
-
-// shared-memory loads / stores by 32-bit shared-window address
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
-}
 
 }  // namespace ptx
 }  // namespace la
