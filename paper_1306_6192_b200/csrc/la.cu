@@ -195,7 +195,9 @@ la_status split_a(int64_t n, int64_t m, const float *A, const Operands &ops, cud
     if (ts != LA_OK) return ts;
     if (m % 4 == 0) {
         const int64_t count4 = n * m / 4;
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, (int64_t)g_state.sms * 8));
+        const int64_t per_block = 256 * SPLIT_UNROLL;
+        const int blocks =
+            (int)std::max<int64_t>(1, std::min<int64_t>((count4 + per_block - 1) / per_block, (int64_t)g_state.sms * 8));
         if (ops.passes == 3)
             split_rows_vec4_kernel<3><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(A),
                                                               reinterpret_cast<float4 *>(ops.a_hi),
@@ -253,7 +255,9 @@ static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const floa
         test_hook("LA_SPLIT_SEPARATE", 0) != 0)
         return false;
     const int64_t count4 = n * m / 4;
-    const int64_t na = std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, (int64_t)g_state.sms * 8));
+    const int64_t per_block = 256 * SPLIT_UNROLL;
+    const int64_t na =
+        std::max<int64_t>(1, std::min<int64_t>((count4 + per_block - 1) / per_block, (int64_t)g_state.sms * 8));
     const int64_t nbx = (p + 63) / 64, nby = (ops.mp + 63) / 64;
     if (na + nbx * nby > INT32_MAX) return false;
     cudaEvent_t t0;

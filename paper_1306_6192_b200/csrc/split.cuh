@@ -35,27 +35,43 @@ __device__ __forceinline__ void split_store(float x, float *hi, float *lo, int64
     if constexpr (PASSES == 3) lo[off] = lo_part(x, h);
 }
 
-// Row-major A, m % 4 == 0: flat float4 grid-stride loop (mp == m).
+// Row-major A, m % 4 == 0: flat float4 grid-stride loop (mp == m), four
+// independent 16-byte loads in flight per thread before any store (a small
+// split is latency-bound: the launch sizes the grid so one batch covers it).
+constexpr int SPLIT_UNROLL = 4;
+
+template <int PASSES>
+__device__ __forceinline__ void split4_store(float4 x, float4 *__restrict__ hi, float4 *__restrict__ lo, int64_t i) {
+    float4 h;
+    h.x = ptx::to_tf32_rna(x.x);
+    h.y = ptx::to_tf32_rna(x.y);
+    h.z = ptx::to_tf32_rna(x.z);
+    h.w = ptx::to_tf32_rna(x.w);
+    __stcg(hi + i, h);
+    if constexpr (PASSES == 3) {
+        float4 l;
+        l.x = lo_part(x.x, h.x);
+        l.y = lo_part(x.y, h.y);
+        l.z = lo_part(x.z, h.z);
+        l.w = lo_part(x.w, h.w);
+        __stcg(lo + i, l);
+    }
+}
+
 template <int PASSES>
 __device__ __forceinline__ void split_rows_vec4_body(const float4 *__restrict__ a, float4 *__restrict__ hi,
                                                     float4 *__restrict__ lo, int64_t count4, int64_t block,
                                                     int64_t nblocks) {
-    for (int64_t i = block * (int64_t)blockDim.x + threadIdx.x; i < count4; i += nblocks * blockDim.x) {
-        const float4 x = __ldcs(a + i);
-        float4 h, l;
-        h.x = ptx::to_tf32_rna(x.x);
-        h.y = ptx::to_tf32_rna(x.y);
-        h.z = ptx::to_tf32_rna(x.z);
-        h.w = ptx::to_tf32_rna(x.w);
-        __stcg(hi + i, h);
-        if constexpr (PASSES == 3) {
-            l.x = lo_part(x.x, h.x);
-            l.y = lo_part(x.y, h.y);
-            l.z = lo_part(x.z, h.z);
-            l.w = lo_part(x.w, h.w);
-            __stcg(lo + i, l);
-        }
+    const int64_t stride = nblocks * blockDim.x;
+    int64_t i = block * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + (SPLIT_UNROLL - 1) * stride < count4; i += SPLIT_UNROLL * stride) {
+        float4 x[SPLIT_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SPLIT_UNROLL; u++) x[u] = __ldcs(a + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < SPLIT_UNROLL; u++) split4_store<PASSES>(x[u], hi, lo, i + u * stride);
     }
+    for (; i < count4; i += stride) split4_store<PASSES>(__ldcs(a + i), hi, lo, i);
 }
 
 template <int PASSES>
