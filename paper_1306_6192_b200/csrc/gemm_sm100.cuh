@@ -62,6 +62,7 @@ constexpr int NUM_THREADS = 32 * (NUM_CTRL_WARPS + NUM_EPI_WARPS);
 constexpr int LAUNCH_REGS = 168;
 constexpr int CTRL_REGS = 56;
 constexpr int EPI_REGS = 216;
+constexpr bool SIGN_CENTRE = true;  // sign-centred promotion chunks (epilogue, below)
 static_assert(32 * NUM_CTRL_WARPS * CTRL_REGS + 32 * NUM_EPI_WARPS * EPI_REGS <= NUM_THREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds the CTA's register pool");
 
@@ -77,6 +78,7 @@ struct GemmArgs {
     int64_t cstride, half_rows, half_off;
     int32_t num_kb;     // K-blocks of BK
     int32_t kc;         // K-blocks per TMEM chunk (promotion interval); >= num_kb: no promotion
+    int32_t center_kb;  // sign-centred chunks only end at or before this K-block; 0: off (ChunkPlan)
     int32_t tiles_m, tiles_n, group_m;
     // Work items: items [0, full_items) are whole tiles in raster order; the
     // remaining tiles (the last, partial wave) are split into two half-width
@@ -215,6 +217,44 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
     tm = first + r % gsz;
     tn = r / gsz;
 }
+
+// Promotion chunks of one work item (nkb K-blocks, interval kc).  Without
+// promotion (kc >= nkb) one chunk.  With sign-centring (kc >= 2) the first two
+// chunks are f = kc/2 K-blocks (they carry no offset: nothing is known about
+// the sums yet, and a short chunk's truncation bias is small), then chunks of
+// kc; the offset for chunk j >= 2 comes from chunk j-2, scaled by kc / len.
+// Both the MMA warp and the epilogue walk the item with this plan.
+struct ChunkPlan {
+    int nkb, kc, f;
+    bool sc;  // sign-centred: chunks >= 2 accumulate onto a preloaded offset
+    __device__ __forceinline__ ChunkPlan(int nkb_, int kc_, bool center) : nkb(nkb_), kc(kc_) {
+        sc = SIGN_CENTRE && center && kc >= 2 && kc < nkb;
+        f = sc ? kc / 2 : kc;
+    }
+    __device__ __forceinline__ int count() const {
+        if (kc >= nkb) return 1;
+        return sc ? 2 + (nkb - 2 * f + kc - 1) / kc : (nkb + kc - 1) / kc;
+    }
+    __device__ __forceinline__ int start(int j) const { return j < 2 ? j * f : 2 * f + (j - 2) * kc; }
+    __device__ __forceinline__ int len(int j) const {
+        const int s0 = start(j);
+        return min(j < 2 ? f : kc, nkb - s0);
+    }
+    // K-block rel of the item: its chunk and whether it opens / closes it
+    __device__ __forceinline__ void at(int rel, int &ci, bool &first, bool &last) const {
+        if (rel < 2 * f) {
+            ci = rel / f;
+            first = rel % f == 0;
+            last = rel % f == f - 1;
+        } else {
+            const int r2 = rel - 2 * f;
+            ci = 2 + r2 / kc;
+            first = r2 % kc == 0;
+            last = r2 % kc == kc - 1;
+        }
+        last = last || rel == nkb - 1;
+    }
+};
 
 // Work item w -> tile (tm, tn), part (-1 = whole tile, 0/1 = column half) and
 // its K-block range [kb0, kb1) and split index ks.
@@ -444,10 +484,14 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint32_t idesc = t < args.full_items ? idesc_full : idesc_half;
             int tm_, tn_, part_, kb0, kb1, ks_;
             decode_item(t, args, tm_, tn_, part_, kb0, kb1, ks_);
+            const ChunkPlan plan(kb1 - kb0, kc, args.center_kb > 0);
             for (int kb = kb0; kb < kb1; kb++) {
-                const int kin = (kb - kb0) % kc;
-                const bool chunk_first = kin == 0;
-                const bool chunk_last = kin == kc - 1 || kb == kb1 - 1;
+                int ci;
+                bool chunk_first, chunk_last;
+                plan.at(kb - kb0, ci, chunk_first, chunk_last);
+                // sign-centred chunks accumulate onto the offset the epilogue
+                // preloaded into the buffer
+                const bool preloaded = plan.sc && ci >= 2;
                 if (chunk_first) {
                     if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[buf], aph ^ 1);
                     else ptx::mbar_wait(&tempty[buf], aph ^ 1);
@@ -471,7 +515,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         const uint32_t ob = (j / JA) * Cfg::B_ATOM + 32 * (j % JA);
                         const uint64_t dah = ptx::sdesc_kmajor<Cfg::ATOM_K>(ah + oa);
                         const uint64_t dbh = ptx::sdesc_kmajor<Cfg::ATOM_K>(bh + ob);
-                        const uint32_t acc = (chunk_first && j == 0) ? 0u : 1u;
+                        const uint32_t acc = (chunk_first && j == 0 && !preloaded) ? 0u : 1u;
                         if constexpr (PASSES == 3) {
                             const uint64_t dal = ptx::sdesc_kmajor<Cfg::ATOM_K>(al + oa);
                             const uint64_t dbl = ptx::sdesc_kmajor<Cfg::ATOM_K>(bl + ob);
@@ -510,7 +554,8 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int t = cluster_id; t < num_items; t += num_clusters) {
             int tm, tn, part, kb0, kb1, ks;
             decode_item(t, args, tm, tn, part, kb0, kb1, ks);
-            const int nchunks = (kb1 - kb0 + kc - 1) / kc;
+            const ChunkPlan plan(kb1 - kb0, kc, args.center_kb > 0);
+            const int nchunks = kb1 > kb0 ? plan.count() : 0;
             float *cbase = args.ksplit > 1 ? args.partial + (int64_t)ks * args.n * args.ldc : nullptr;
             // whole tile: this warp owns columns [half*BN/2, +BN/2); half item: [half*BN/4, +BN/4)
             const int cpw = part < 0 ? Cfg::COLS_PER_WARP : Cfg::COLS_PER_WARP / 2;
@@ -550,14 +595,29 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 buf ^= 1;
                 if (buf == 0) aph ^= 1;
             } else {
-                // accumulator promotion: fp32 (RN) running sum of TMEM chunks
+                // accumulator promotion: fp32 (RN) running sum of TMEM chunks.
+                // Sign-centred chunks: the accumulator truncates toward zero, so
+                // a chunk whose partial sums keep one sign is biased toward zero
+                // (same-sign data: 1.68 x 2^-20 S at K = 16384).  After draining
+                // chunk c, if this thread's chunk values x (its row, BN/2
+                // columns) all share one sign, the offset -x_min/2 (x_min: the
+                // value of smallest magnitude, so no partial sum exceeds |x|) is
+                // written into the buffer for chunk c+2, which the MMA then
+                // accumulates onto: the partial sums start on the other side of
+                // zero and cross it, and truncations up and down cancel (0.96 x
+                // 2^-20 S at K = 16384).  Drained values are x = R - off; mixed
+                // signs give off = 0 and the same bits as plain promotion.  Exact
+                // on integer data: off is half an integer chunk sum and |R| <= |x|.
                 float acc[Cfg::PIECES][32];
+                float off_cur = 0.0f, off_oth = 0.0f;  // offsets preloaded in this / the other buffer
 #pragma unroll 1
                 for (int c = 0; c < nchunks; c++) {
                     ptx::mbar_wait(&tfull[buf], aph);
                     if (e == 0 && lane == 0 && !traced_epi) { trace_stamp(args.trace, 5); traced_epi = true; }
                     ptx::tc_fence_after();
                     const uint32_t taddr = tq + buf * BN;
+                    const bool refill = plan.sc && c + 2 < nchunks;  // this buffer holds chunk c+2 next
+                    float lo = __uint_as_float(0x7f800000u), hi = -lo;   // chunk values' range (this row)
                     // two 32-column loads in flight per wait (the drain's latency
                     // bounds how short a chunk can be without stalling the MMAs)
 #pragma unroll
@@ -577,19 +637,53 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                                 }
                             } else {
 #pragma unroll
-                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v0[i]);
+                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v0[i]) - off_cur;
                                 if (two) {
 #pragma unroll
-                                    for (int i = 0; i < 32; i++) acc[qq + 1][i] += __uint_as_float(v1[i]);
+                                    for (int i = 0; i < 32; i++) acc[qq + 1][i] += __uint_as_float(v1[i]) - off_cur;
+                                }
+                            }
+                            if (refill) {
+#pragma unroll
+                                for (int i = 0; i < 32; i++) {
+                                    lo = fminf(lo, __uint_as_float(v0[i]));
+                                    hi = fmaxf(hi, __uint_as_float(v0[i]));
+                                }
+                                if (two) {
+#pragma unroll
+                                    for (int i = 0; i < 32; i++) {
+                                        lo = fminf(lo, __uint_as_float(v1[i]));
+                                        hi = fmaxf(hi, __uint_as_float(v1[i]));
+                                    }
                                 }
                             }
                         }
+                    }
+                    // the range of x = v - off_cur is [lo - off_cur, hi - off_cur]
+                    float off_new = 0.0f;
+                    if (refill) {
+                        lo -= off_cur;
+                        hi -= off_cur;
+                        // chunk c+2 is a full chunk of kc inside the centring range:
+                        // half the smallest-magnitude value, scaled from this chunk's
+                        // length (f or kc) to kc
+                        const int c2 = c + 2;
+                        if (plan.len(c2) == kc && kb0 + plan.start(c2) + kc <= args.center_kb) {
+                            const float scale = -0.5f * (float)kc / (float)plan.len(c);
+                            off_new = lo > 0.0f ? scale * lo : (hi < 0.0f ? scale * hi : 0.0f);
+                        }
+#pragma unroll
+                        for (int qq = 0; qq < Cfg::PIECES; qq++)
+                            if (qq < pieces) ptx::tmem_st_32x32b_x32_bcast(taddr + qq * 32, __float_as_uint(off_new));
+                        ptx::tmem_st_wait();
                     }
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     buf ^= 1;
                     if (buf == 0) aph ^= 1;
+                    off_cur = off_oth;
+                    off_oth = off_new;
                 }
 #pragma unroll
                 for (int qq = 0; qq < Cfg::PIECES; qq++) {

@@ -338,6 +338,16 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     if (pk < 0) pk = km <= 64 ? 32 : (km <= 192 ? 64 : 128);
     args.kc = pk <= 0 ? args.num_kb : (int32_t)std::max<int64_t>(1, (pk + KB - 1) / KB);
     if (args.kc > args.num_kb) args.kc = args.num_kb;
+    // Sign-centred promotion chunks (gemm_sm100.cuh ChunkPlan) end within the
+    // policy K (la_cgemm: the real half of its 2m-long embedding, so
+    // zero-imaginary products keep la_gemm's bits), and only when K spans at
+    // least 8 chunks: an offset is extrapolated from the chunk two before, so a
+    // sign change along K can enlarge one chunk's partial sums -- diluted over
+    // >= 8 chunks, not over 2 or 3 (K = 256 with sign-flipped halves: 0.70 ->
+    // 1.71 x 2^-20 S against the exact product when centred).
+    const int64_t policy_kb = (km + KB - 1) / KB;
+    args.center_kb = args.kc >= 2 && policy_kb >= 8 * (int64_t)args.kc
+                         ? (int32_t)std::min<int64_t>(args.num_kb, policy_kb) : 0;
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
     args.group_m = (int32_t)std::max<int64_t>(1, diag_knob("LA_GROUP_M", 8));
