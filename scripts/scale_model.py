@@ -129,24 +129,35 @@ for g in (2, 4, 8):
     best = None
     result["g"][g] = {}
     for name, ws in plans(p).items():
-        t_comm = 0.0
-        t_comp = sa
-        for c, w in enumerate(ws):
-            last = c == len(ws) - 1
-            key = (rows, w, not last)
-            if key not in cache:
-                cache[key] = gemm_time(rows, w, not last)
-            s, gm = cache[key]
-            sb = max(0.0, s - sa)   # this launch also split A_r, which the multi path does once
-            bytes_ = 4.0 * m * w
-            t_comm += (bytes_ / pack_gbs / 1e9 + bytes_ / BW + CALL_US * 1e-6) * 1e3
-            t_comp = max(t_comp, t_comm) + sb + gm
-        eff = T1 / (g * t_comp)
-        result["g"][g][name] = {"widths": ws, "ms": t_comp, "efficiency": eff}
-        print(f"g={g} rows={rows:5d} {name:16s} panels={len(ws)} ms={t_comp:7.3f} eff={100 * eff:5.1f}%  {ws}",
-              flush=True)
-        if best is None or eff > best[1]:
-            best = (name, eff)
+        for dist in (False, True):
+            # dist: the root scatters 1/g of each raw panel, every rank splits
+            # its slice and the hi/lo slices are all-gathered (8 bytes per
+            # element arrive instead of 4; the split work per rank is 1/g)
+            t_comm = 0.0
+            t_comp = sa
+            for c, w in enumerate(ws):
+                last = c == len(ws) - 1
+                key = (rows, w, not last)
+                if key not in cache:
+                    cache[key] = gemm_time(rows, w, not last)
+                s, gm = cache[key]
+                sb = max(0.0, s - sa)   # this launch also split A_r, which the multi path does once
+                if dist:
+                    raw = 4.0 * m * w
+                    t_comm += (raw / pack_gbs / 1e9 + raw / g / BW + 8.0 * m * w * (g - 1) / g / BW +
+                               2 * CALL_US * 1e-6 + sb / g * 1e-3) * 1e3
+                    t_comp = max(t_comp, t_comm) + gm
+                else:
+                    bytes_ = 4.0 * m * w
+                    t_comm += (bytes_ / pack_gbs / 1e9 + bytes_ / BW + CALL_US * 1e-6) * 1e3
+                    t_comp = max(t_comp, t_comm) + sb + gm
+            eff = T1 / (g * t_comp)
+            label = name + (" dist-split" if dist else "")
+            result["g"][g][label] = {"widths": ws, "ms": t_comp, "efficiency": eff}
+            print(f"g={g} rows={rows:5d} {label:27s} panels={len(ws)} ms={t_comp:7.3f} eff={100 * eff:5.1f}%  {ws}",
+                  flush=True)
+            if best is None or eff > best[1]:
+                best = (label, eff)
     result["g"][g]["best"] = best
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out", "scale_model.json")
 os.makedirs(os.path.dirname(out), exist_ok=True)

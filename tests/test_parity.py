@@ -260,6 +260,14 @@ def test_config4_16384_sampled(la, kind):
     _sampled_check(la, 16384, 16384, 16384, kind)
 
 
+def test_config4_16384_plain_tf32_kb64_sampled(la):
+    """Plain TF32 at n = 16384 runs the 64-wide K-block kernel (dispatched from
+    2^41 multiply-adds, la.cu gemm_run): sampled elements against the oracle
+    within the north_star's 2^-9 bound (elsewhere the KB=64 kernel is only
+    compared bitwise with the KB=32 one)."""
+    _sampled_check(la, 16384, 16384, 16384, "random", "tf32")
+
+
 def test_config4_16384_integer_freivalds(la):
     _sampled_check(la, 16384, 16384, 16384, "integer", freivalds=True)
 
