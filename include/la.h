@@ -85,7 +85,8 @@ typedef enum {
     /* Upper bound on the number of SMs the GEMM kernel occupies (0 = all).  The
      * multi-GPU path uses it to leave SMs for NCCL. */
     LA_OPT_MAX_SMS = 1,
-    /* Number of N-panels B is broadcast in by la_gemm_multi (>= 1). */
+    /* N-panels B is broadcast in by la_gemm_multi: 0 (default) = the plan of
+     * la_panel_plan's timeline model, >= 1 = that many equal panels. */
     LA_OPT_PANELS = 2,
     /* 1: record CUDA events around every split and GEMM launch so that
      * la_kernel_times() can report their device durations (bench.py's
@@ -229,6 +230,16 @@ LA_API la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A
  * SURVEY 8(f)).  Freed by the next call, la_comm_init or la_finalize.
  * Errors: NOT_INITIALIZED, INVALID_VALUE, NCCL. */
 LA_API la_status la_gather_alloc(int64_t bytes, void **d_out);
+
+/* Column panels la_gemm_multi broadcasts B in (pure host arithmetic, no
+ * device needed): widths[0 .. *count) sum to p, multiples of 256 except the
+ * last.  panels > 0: that many equal panels; panels == 0: the plan a timeline
+ * model of one rank (broadcast of panel c overlapping the GEMM of panel c-1,
+ * replicated split, wave quantisation on sms - reserved SMs) scores best among
+ * equal and geometric (narrow first panel) plans.  Errors: INVALID_VALUE (bad
+ * sizes, more than max_panels panels). */
+LA_API la_status la_panel_plan(int64_t n, int64_t m, int64_t p, int ngpu, int sms, int reserved, int64_t panels,
+                               int64_t *widths, int max_panels, int *count);
 
 /* Rows owned by `rank` of g: [*row0, *row0 + *rows).  Pure host arithmetic. */
 LA_API la_status la_shard_rows(int64_t n, int rank, int ngpu, int64_t *row0, int64_t *rows);

@@ -29,7 +29,8 @@ OPTIONS = {"promote_k": 0, "max_sms": 1, "panels": 2, "kernel_timing": 3, "nccl_
 EXPORTS = ("la_init", "la_set_mode", "la_set_option", "la_get_option", "la_gemm", "la_gemm_host",
            "la_get_unique_id", "la_comm_init", "la_gemm_multi", "la_shard_rows", "la_finalize",
            "la_status_string", "la_last_error", "la_last_launch_count", "la_kernel_times", "la_cgemm",
-           "la_add", "la_dgemm", "la_gather_alloc", "la_gemm_host_batch", "la_comm_size")
+           "la_add", "la_dgemm", "la_gather_alloc", "la_gemm_host_batch", "la_comm_size",
+           "la_panel_plan")
 
 
 class LaError(RuntimeError):
@@ -60,6 +61,8 @@ def _load() -> ctypes.CDLL:
         "la_comm_size": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], st),
         "la_gemm_multi": ([i64, i64, i64, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp], st),
         "la_shard_rows": ([i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)], st),
+        "la_panel_plan": ([i64, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, ctypes.POINTER(i64),
+                           ctypes.c_int, ctypes.POINTER(ctypes.c_int)], st),
         "la_finalize": ([], st),
         "la_status_string": ([ctypes.c_int], ctypes.c_char_p),
         "la_last_error": ([], ctypes.c_char_p),
@@ -284,6 +287,17 @@ def shard_rows(n: int, rank: int, ngpu: int):
     r0, r = ctypes.c_int64(), ctypes.c_int64()
     _check(_lib.la_shard_rows(int(n), int(rank), int(ngpu), ctypes.byref(r0), ctypes.byref(r)), "la_shard_rows")
     return r0.value, r.value
+
+
+def panel_plan(n: int, m: int, p: int, ngpu: int, sms: int = 148, reserved: int = 8, panels: int = 0):
+    """Column-panel widths la_gemm_multi broadcasts B in (la_panel_plan; host
+    arithmetic, no GPU needed)."""
+    cap = 64
+    w = (ctypes.c_int64 * cap)()
+    cnt = ctypes.c_int()
+    _check(_lib.la_panel_plan(int(n), int(m), int(p), int(ngpu), int(sms), int(reserved), int(panels), w, cap,
+                              ctypes.byref(cnt)), "la_panel_plan")
+    return [w[i] for i in range(cnt.value)]
 
 
 _COMM = {}   # this process's rank in the library communicator (binding-side shape checks)

@@ -741,7 +741,7 @@ la_status la_set_option(la_option option, int64_t value) {
             g_state.max_sms = value;
             return LA_OK;
         case LA_OPT_PANELS:
-            if (value < 1) return fail(LA_ERR_INVALID_VALUE, "panels must be >= 1");
+            if (value < 0) return fail(LA_ERR_INVALID_VALUE, "panels must be >= 0 (0: automatic)");
             g_state.panels = value;
             return LA_OK;
         case LA_OPT_KERNEL_TIMING:

@@ -22,7 +22,7 @@ struct State {
     // tcgen05 kind::tf32 accumulator truncates (probes in tests/test_probe.py).
     int64_t promote_k = -1;  // -1: automatic by K (launch_gemm)
     int64_t max_sms = 0;
-    int64_t panels = 4;
+    int64_t panels = 0;      // la_gemm_multi N-panels: 0 = la_panel_plan's model
     int64_t nccl_sms = 8;    // SMs left to NCCL (ncclConfig_t.maxCTAs) while B panels are in flight
     int last_launches = 0;
     void *staging = nullptr;  // la_gemm_host device staging
@@ -56,6 +56,7 @@ la_status fail(la_status s, const char *fmt, ...);
 //   LA_HOST_PANELS=q       host transfer panels                (tests/test_parity.py)
 //   LA_DGEMM_CPASYNC=1     cp.async DGEMM instead of TMA       (tests/test_parity_ext.py)
 //   LA_TEST_GATHER_ROW0=r  fused-gather destination row, 1 rank (tests/test_multi.py)
+//   LA_TEST_PLAN_NGPU=g    panel plan of g ranks, 1 rank         (tests/test_multi.py)
 //   LA_TEST_GATHER_PEERS=g, LA_TEST_GATHER_STRIDE=s  one rank emulating g ranks'
 //                          C_full copies at float offsets 0, s, 2s.. of its own
 //                          window (tests/test_multi.py)

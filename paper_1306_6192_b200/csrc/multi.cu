@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -91,6 +92,63 @@ la_status comm_destroy() {
 // (LA_OPT_NCCL_SMS, default 8; read by la_comm_init for ncclConfig_t.maxCTAs).
 static int reserved_sms() { return (int)std::max<int64_t>(0, g_state.nccl_sms); }
 
+// ---- panel plan (la_panel_plan) -------------------------------------------
+// B travels in column panels; panel c's GEMM starts when panel c has arrived
+// and panel c-1's GEMM is done.  A timeline model scores candidate plans:
+//   broadcast  4 m w / link + 25 us per call (+ the root's pack copy),
+//   split      12 m w bytes of HBM traffic per panel (replicated on every rank),
+//   GEMM       waves x one 256 x 256 tile's time, waves counted on the clusters
+//              the launch gets (SMs - reserved for all but the last panel), with
+//              the half-width tail items of launch_gemm (a last wave at most
+//              half full costs half a wave).
+// Rates: tile time from the measured single-GPU kernel (793 TFLOP/s issued
+// over 74 clusters, 3xTF32), link 700 GB/s (B200_PROFILING: 770 GB/s peer copy),
+// HBM 6 TB/s.  Candidates: 1, 2, 4, 8, 16 equal panels and geometric plans
+// (first panel 256 .. 2048 columns, each next one 2x or 3x wider) -- a narrow
+// first panel shortens the broadcast nothing can overlap.  Widths are
+// multiples of 256 (the CTA pair's N tile) except the last.
+namespace {
+struct PlanModel {
+    double rows, m, t_tile, link, hbm;
+    int clusters_all, clusters_capped;
+    double waves(double tiles, int W) const {
+        const double full = std::floor(tiles / W), r = tiles - full * W;
+        if (r <= 0) return full;
+        return full + ((2 * r <= W && tiles > W) ? 0.5 : 1.0);
+    }
+    double time(const std::vector<int64_t> &ws) const {
+        double comm = 0, comp = 12.0 * rows * m / hbm;  // split of A_r
+        for (size_t c = 0; c < ws.size(); c++) {
+            const double w = (double)ws[c];
+            comm += 4.0 * m * w / link + 25e-6 + 8.0 * m * w / (3 * hbm);
+            const double tiles = std::ceil(rows / 256.0) * std::ceil(w / 256.0);
+            const int W = c + 1 < ws.size() ? clusters_capped : clusters_all;
+            comp = std::max(comp, comm) + 12.0 * m * w / hbm + 5e-6 + waves(tiles, W) * t_tile;
+        }
+        return comp;
+    }
+};
+std::vector<int64_t> equal_plan(int64_t p, int64_t P) {
+    int64_t w = (p + P - 1) / P;
+    w = (w + 255) / 256 * 256;
+    std::vector<int64_t> ws;
+    for (int64_t j = 0; j < p; j += w) ws.push_back(std::min(w, p - j));
+    return ws;
+}
+std::vector<int64_t> geometric_plan(int64_t p, int64_t first, int64_t grow) {
+    std::vector<int64_t> ws;
+    int64_t j = 0, w = first;
+    while (j < p) {
+        int64_t ww = std::min(w, p - j);
+        if (p - j - ww < first) ww = p - j;  // no sliver at the end
+        ws.push_back(ww);
+        j += ww;
+        w = (w * grow + 255) / 256 * 256;
+    }
+    return ws;
+}
+}  // namespace
+
 }  // namespace la
 
 using namespace la;
@@ -147,6 +205,46 @@ la_status la_comm_size(int *nranks, int *rank) {
     return LA_OK;
 }
 
+la_status la_panel_plan(int64_t n, int64_t m, int64_t p, int ngpu, int sms, int reserved, int64_t panels,
+                        int64_t *widths, int max_panels, int *count) {
+    if (n <= 0 || m <= 0 || p <= 0 || ngpu < 1 || sms < 2 || reserved < 0 || panels < 0 || !widths || !count ||
+        max_panels < 1)
+        return fail(LA_ERR_INVALID_VALUE, "bad panel-plan arguments");
+    std::vector<int64_t> best;
+    if (panels > 0) {
+        best = equal_plan(p, panels);
+    } else if (ngpu == 1) {
+        best = {p};  // nothing to overlap: one panel
+    } else {
+        PlanModel pm;
+        pm.rows = (double)((n + ngpu - 1) / ngpu);
+        pm.m = (double)m;
+        pm.clusters_all = std::max(1, sms / 2);
+        pm.clusters_capped = std::max(1, (sms - reserved) / 2);
+        pm.t_tile = 6.0 * 256.0 * 256.0 * (double)m / (793e12 / 74.0);
+        pm.link = 700e9;
+        pm.hbm = 6e12;
+        double bt = 0;
+        auto consider = [&](const std::vector<int64_t> &ws) {
+            if ((int)ws.size() > max_panels) return;
+            const double t = pm.time(ws);
+            if (best.empty() || t < bt) {
+                best = ws;
+                bt = t;
+            }
+        };
+        for (int64_t P : {1, 2, 4, 8, 16}) consider(equal_plan(p, P));
+        for (int64_t first : {256, 512, 1024, 2048})
+            for (int64_t grow : {2, 3})
+                if (first < p) consider(geometric_plan(p, first, grow));
+    }
+    if ((int)best.size() > max_panels)
+        return fail(LA_ERR_INVALID_VALUE, "%zu panels exceed the caller's %d", best.size(), max_panels);
+    for (size_t c = 0; c < best.size(); c++) widths[c] = best[c];
+    *count = (int)best.size();
+    return LA_OK;
+}
+
 la_status la_gather_alloc(int64_t bytes, void **d_out) {
     std::lock_guard<std::recursive_mutex> lk(g_mutex);
     if (!g_state.initialized) return fail(LA_ERR_NOT_INITIALIZED, "la_init has not been called");
@@ -194,11 +292,20 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
     la_shard_rows(n, rank, ngpu, &row0, &rows);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-    // N-panels: widths are multiples of 128 (the GEMM's N tile) except the last.
-    int64_t P = std::max<int64_t>(1, g_state.panels);
-    int64_t pc = (p + P - 1) / P;
-    pc = (pc + 127) / 128 * 128;
-    P = (p + pc - 1) / pc;
+    // N-panels (la_panel_plan): LA_OPT_PANELS = 0 (default) lets the timeline
+    // model choose, > 0 forces that many equal panels.
+    std::vector<int64_t> widths(64);
+    int P32 = 0;
+    {
+        // test hook (one rank): plan the panels as for LA_TEST_PLAN_NGPU ranks
+        const int plan_g = ngpu == 1 ? (int)std::max<int64_t>(1, test_hook("LA_TEST_PLAN_NGPU", 1)) : ngpu;
+        la_status ps = la_panel_plan(n, m, p, plan_g, g_state.sms, reserved_sms(), g_state.panels, widths.data(),
+                                     (int)widths.size(), &P32);
+        if (ps != LA_OK) return ps;
+    }
+    const int64_t P = P32;
+    std::vector<int64_t> col0(P + 1, 0);
+    for (int64_t c = 0; c < P; c++) col0[c + 1] = col0[c] + widths[c];
     while ((int64_t)g_comm.panel_ready.size() < P) {
         cudaEvent_t e;
         LA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -273,7 +380,7 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
                               g_comm.stream));
     }
     for (int64_t c = 0; c < P; c++) {
-        const int64_t j0 = c * pc, w = std::min(pc, p - j0);
+        const int64_t j0 = col0[c], w = widths[c];
         float *panel = bstage + m * j0;  // packed m x w panel
         if (rank == root) {
             if (P == 1) {
@@ -292,7 +399,7 @@ la_status la_gemm_multi(int64_t n, int64_t m, int64_t p, const float *d_A_local,
     la_status s = split_a(rows, m, d_A_local, ops, st, &launches);
     const int reserve = ngpu > 1 ? reserved_sms() : 0;
     for (int64_t c = 0; c < P && s == LA_OK; c++) {
-        const int64_t j0 = c * pc, w = std::min(pc, p - j0);
+        const int64_t j0 = col0[c], w = widths[c];
         LA_CK(cudaStreamWaitEvent(st, g_comm.panel_ready[c], 0));
         s = split_b(m, j0, w, bstage + m * j0, w, ops, st, &launches);
         if (s != LA_OK) break;

@@ -119,6 +119,12 @@ def plans(pw):
     return out
 
 
+def plans_for(g):
+    out = plans(p)
+    out["la_panel_plan (default)"] = la.panel_plan(n, m, p, g, sms, RESERVE)
+    return out
+
+
 cache = {}
 result = {"n": n, "T1_ms": T1, "bw_model_gbs": BW / 1e9, "pack_gbs": pack_gbs, "nccl_sms": RESERVE, "g": {}}
 print(f"n={n}: T1 = {T1:.2f} ms ({2 * n ** 3 / T1 / 1e9:.1f} TFLOP/s); broadcast modelled at {BW / 1e9:.0f} GB/s "
@@ -128,7 +134,7 @@ for g in (2, 4, 8):
     sa, _ = timed(lambda: la.gemm(A[:rows], B[:, :4].contiguous(), out=torch.empty(rows, 4, device="cuda")))
     best = None
     result["g"][g] = {}
-    for name, ws in plans(p).items():
+    for name, ws in plans_for(g).items():
         for dist in (False, True):
             # dist: the root scatters 1/g of each raw panel, every rank splits
             # its slice and the hi/lo slices are all-gathered (8 bytes per

@@ -18,7 +18,7 @@ def _declared():
 def test_header_and_binding_agree():
     import paper_1306_6192_b200 as la
     declared = _declared()
-    assert len(declared) == 21
+    assert len(declared) == 22
     assert sorted(declared) == sorted(la.EXPORTS)
 
 
@@ -61,7 +61,7 @@ def test_not_initialized_and_argument_errors():
     assert lib.la_gemm_multi(4, 4, 4, 16, 32, 64, None, 0, 1, None) == la.LA_ERR_NOT_INITIALIZED
     assert lib.la_set_mode(7) == la.LA_ERR_INVALID_VALUE
     assert lib.la_set_option(99, 1) == la.LA_ERR_INVALID_VALUE
-    assert lib.la_set_option(la.OPTIONS["panels"], 0) == la.LA_ERR_INVALID_VALUE
+    assert lib.la_set_option(la.OPTIONS["panels"], -1) == la.LA_ERR_INVALID_VALUE
     # no device in this container: la_init reports it instead of crashing
     assert lib.la_init(0) in (la.LA_ERR_INVALID_VALUE, la.LA_ERR_CUDA)
     import ctypes

@@ -110,4 +110,4 @@ def test_multi_panel_guards(la, monkeypatch):
         monkeypatch.setenv("LA_SPLIT_K", "0")
         assert torch.equal(C, la.gemm(A, B))
     finally:
-        la.set_option("panels", 4)
+        la.set_option("panels", 0)

@@ -81,7 +81,36 @@ def la1():
     la.init(0)
     la.comm_init(la.get_unique_id(), 0, 1)
     yield la
-    la.set_option("panels", 4)
+    la.set_option("panels", 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,p,g", [(4096, 2048, 8192, 2), (8192, 2048, 8192, 2), (2048, 8192, 8192, 8)])
+def test_multi_model_panel_plan_bitwise(la1, n, m, p, g, monkeypatch):
+    """The timeline model's unequal panels (narrow first panel, wider later
+    ones: planned as for g ranks through LA_TEST_PLAN_NGPU) executed with one
+    rank: bitwise equal to la_gemm without split-K, and integer inputs equal to
+    the oracle on sampled elements."""
+    import oracle
+    la = la1
+    la.set_option("panels", 0)
+    ws = la.panel_plan(n, m, p, g)
+    assert len(ws) > 1 and len(set(ws)) > 1, ws
+    monkeypatch.setenv("LA_SPLIT_K", "0")
+    monkeypatch.setenv("LA_TEST_PLAN_NGPU", str(g))
+    for kind in ("stress", "integer"):
+        A, B = inputs.pair(n, m, p, kind, device="cuda")
+        ref = la.gemm(A, B)
+        Cl = torch.empty(n, p, device="cuda")
+        la.gemm_multi(n, m, p, A, B, Cl, None, root=0, ngpu=1)
+        torch.cuda.synchronize()
+        assert torch.equal(Cl, ref)
+        if kind == "integer":
+            rows = np.linspace(0, n - 1, 16).astype(np.int64)
+            cols = np.unique(np.concatenate([np.cumsum([0] + ws[:-1]), np.linspace(0, p - 1, 24).astype(np.int64)]))
+            got = Cl.cpu().numpy()[rows][:, cols]
+            want = oracle.gemm(A.cpu().numpy()[rows], B.cpu().numpy()[:, cols], threads=8)
+            assert np.array_equal(got, want)
 
 
 @pytest.mark.gpu
@@ -99,9 +128,9 @@ def test_multi_one_rank_bitwise_equals_single(la1, n, m, p, panels, monkeypatch)
     torch.cuda.synchronize()
     assert torch.equal(Cl, ref)
     assert torch.equal(Cf, ref)
-    pc = -(-(-(-p // panels)) // 128) * 128            # panel width: ceil(p / panels) up to 128
-    n_panels = -(-p // pc)
-    assert la.last_launch_count() == 1 + 2 * n_panels   # split A, then split B + GEMM per panel
+    ws = la.panel_plan(n, m, p, 1, panels=panels)    # equal panels, multiples of 256 but the last
+    assert len(ws) == -(-p // (-(-(-(-p // panels)) // 256) * 256))
+    assert la.last_launch_count() == 1 + 2 * len(ws)  # split A, then split B + GEMM per panel
 
 
 @pytest.mark.gpu
@@ -212,3 +241,27 @@ def test_fused_gather_emulated_ranks_vs_oracle(la1, g, kind, monkeypatch):
         else:
             assert float((np.abs(copies[pe].astype(np.float64) - ref) / S).max()) <= 2.0 ** -20, pe
     assert np.array_equal(copies[0], copies[g - 1])
+
+
+@pytest.mark.parametrize("n,m,p,g", [(16384, 16384, 16384, 2), (16384, 16384, 16384, 8), (65536, 65536, 65536, 8),
+                                     (1000, 2000, 1500, 2), (4096, 300, 777, 4), (512, 512, 100, 8)])
+def test_panel_plan_host(n, m, p, g):
+    """la_panel_plan (host arithmetic, no GPU): the panels tile B's columns in
+    order, widths are multiples of the 256-wide pair tile except the last, the
+    model-chosen plan never starts with a panel wider than the next one (the
+    first broadcast is the one nothing overlaps), one GPU gets one panel, and a
+    forced count gives equal panels."""
+    import paper_1306_6192_b200 as la
+    ws = la.panel_plan(n, m, p, g)
+    assert sum(ws) == p and all(w > 0 for w in ws)
+    assert all(w % 256 == 0 for w in ws[:-1])
+    if len(ws) > 1:
+        assert ws[0] <= ws[1]
+    assert la.panel_plan(n, m, p, 1) == [p]
+    for P in (1, 3, 4):
+        eq = la.panel_plan(n, m, p, g, panels=P)
+        assert sum(eq) == p and len(eq) <= P and len(set(eq[:-1])) <= 1
+    with pytest.raises(la.LaError):
+        la.panel_plan(n, m, p, g, panels=-1)
+    with pytest.raises(la.LaError):
+        la.panel_plan(0, m, p, g)
