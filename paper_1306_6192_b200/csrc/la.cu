@@ -329,9 +329,10 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // random-sign inputs vs the exact product (scripts/positive_check.py):
     // K = 256 in one chunk 0.79 x 2^-20 S, in two of 128 0.39, in four of 64
     // 0.19; so chunks of 32 up to K = 64 (24-bit inputs at K = 61: 0.58 in one
-    // chunk, 0.27 in two), 64 up to K = 192, 128 up to K = 1024, 256 beyond
-    // (where a finer interval costs 9-24% of throughput and buys nothing on
-    // these inputs).  Chunks of 64 cost ~18% at K = 256, of 32 ~12% at K = 64
+    // chunk, 0.27 in two), 64 up to K = 192, 128 beyond (256 halves the drain
+    // work but doubles the same-sign truncation bias: 2.94 vs 1.68 x 2^-20 S
+    // at K = 16384 before sign-centring, and costs nothing measurable at 128
+    // for n >= 4096).  Chunks of 64 cost ~18% at K = 256, of 32 ~12% at K = 64
     // on 4096-wide outputs (scripts/promote_cost.py).
     int64_t pk = PASSES == 3 ? g_state.promote_k : 0;
     const int64_t km = out.policy_k > 0 ? out.policy_k : m;
