@@ -487,6 +487,26 @@ def test_same_sign_inputs_as_accurate_as_listing1(la, m):
         assert gpu <= 2.0 ** -20, gpu / 2.0 ** -20
 
 
+@pytest.mark.parametrize("n,m,p,sign", [(256, 4096, 256, 1), (256, 4096, 256, -1), (512, 16384, 384, 1),
+                                        (300, 2000, 500, -1)])
+def test_same_sign_integer_inputs_exact(la, n, m, p, sign):
+    """Sign-centred promotion chunks (K spans >= 8 chunks here) on same-sign
+    integer inputs: the preloaded offsets are halves of integer chunk sums, so
+    every partial sum stays exactly representable and the product equals the
+    oracle value for value (split-K on and off)."""
+    A = inputs.generate(n, m, 0, "integer").abs() * sign
+    B = inputs.generate(m, p, 1, "integer").abs()
+    ref = oracle.gemm(A.numpy(), B.numpy(), threads=THREADS)
+    for sk in (None, "0"):
+        if sk is not None:
+            os.environ["LA_SPLIT_K"] = sk
+        try:
+            C = la.gemm(A.cuda(), B.cuda()).cpu().numpy()
+        finally:
+            os.environ.pop("LA_SPLIT_K", None)
+        assert np.array_equal(C, ref)
+
+
 def test_finalize_and_reinit(la):
     """la_finalize releases everything; the library initialises again and
     computes the same product (state, pools, streams, events rebuilt)."""
