@@ -277,16 +277,32 @@ static bool split_ab(int64_t n, int64_t m, int64_t p, const float *A, const floa
 
 // Split-K factor for a launch of `tiles` output tiles over `slots` concurrent
 // clusters: only with few tiles (at most half the slots) and a long K, at least
-// 8 K-blocks per piece, at most 64 pieces (S * tiles <= slots bounds the
-// partial workspace by slots x one tile, whatever S is).
-static int splitk_factor(int64_t tiles, int64_t slots, int num_kb) {
-    const int64_t forced = test_hook("LA_SPLIT_K", -1);
-    if (forced >= 0) return forced <= 1 ? 1 : (int)std::min<int64_t>(forced, 1024);
-    if (2 * tiles > slots || num_kb < 16) return 1;
-    int S = (int)std::min<int64_t>(std::min<int64_t>(slots / tiles, num_kb / 8), 64);
+// `min_piece` K-blocks per piece, at most 64 pieces (S * tiles <= slots bounds
+// the partial workspace by slots x one tile, whatever S is).
+static int splitk_pieces(int64_t tiles, int64_t slots, int num_kb, int min_piece) {
+    if (2 * tiles > slots || num_kb < 2 * min_piece) return 1;
+    int S = (int)std::min<int64_t>(std::min<int64_t>(slots / tiles, num_kb / min_piece), 64);
     if (S <= 1) return 1;
     const int per = (num_kb + S - 1) / S;
     return (num_kb + per - 1) / per;
+}
+
+// Pieces of at least 8 K-blocks; single-CTA launches (cg == 1, whose K-blocks
+// take half the time, so the fixed prologue / epilogue / reduce cost weighs
+// more) go down to 4 while the pieces fill at most 3/4 of the SMs: 512^3 14.7
+// -> 12.2 us per call in a graph, 256x2048x256 16.6 -> 14.3, 128x4096x128
+// 17.1 -> 15.4, 384x1536x384 16.4 -> 14.1, 300x500x200 15.2 -> 12.5; filling
+// the machine with short pieces lost (777x1236x260 19.1 -> 20.8, 147 pieces;
+// 2000x700x300 20.3 -> 21.4, 144), and so did 4 on CTA pairs
+// (scripts/splitk_piece_sweep.py).  The kernel choice (for_choice) prices both
+// kernels with 8.
+static int splitk_factor(int64_t tiles, int64_t slots, int num_kb, int cg, bool for_choice = false) {
+    const int64_t forced = test_hook("LA_SPLIT_K", -1);
+    if (forced >= 0) return forced <= 1 ? 1 : (int)std::min<int64_t>(forced, 1024);
+    const int S8 = splitk_pieces(tiles, slots, num_kb, 8);
+    if (for_choice || cg != 1) return S8;
+    const int S4 = splitk_pieces(tiles, slots, num_kb, (int)std::max<int64_t>(1, diag_knob("LA_SPLITK_MIN_PIECE1", 4)));
+    return 4 * tiles * S4 <= 3 * slots ? S4 : S8;
 }
 
 template <int CG, int BN, int STAGES, int PASSES, int KB = BK>
@@ -347,8 +363,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     // >= 8 chunks, not over 2 or 3 (K = 256 with sign-flipped halves: 0.70 ->
     // 1.71 x 2^-20 S against the exact product when centred).
     const int64_t policy_kb = (km + KB - 1) / KB;
-    args.center_kb = args.kc >= 2 && policy_kb >= 8 * (int64_t)args.kc
-                         ? (int32_t)std::min<int64_t>(args.num_kb, policy_kb) : 0;
+    auto set_center = [&]() {
+        args.center_kb = args.kc >= 2 && policy_kb >= 8 * (int64_t)args.kc
+                             ? (int32_t)std::min<int64_t>(args.num_kb, policy_kb) : 0;
+    };
+    set_center();
     args.tiles_m = (int32_t)((n + Cfg::TILE_M - 1) / Cfg::TILE_M);
     args.tiles_n = (int32_t)((pc + BN - 1) / BN);
     args.group_m = (int32_t)std::max<int64_t>(1, diag_knob("LA_GROUP_M", 8));
@@ -406,13 +425,21 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     void *part_buf = nullptr;
     {
         const int kb32 = (int)((m + 31) / 32);
-        const int S = out.splitk_ok ? splitk_factor(tiles, max_clusters, kb32) : 1;
+        const int S = out.splitk_ok ? splitk_factor(tiles, max_clusters, kb32, CG) : 1;
         if (S > 1) {
             // pieces of kb_per K-blocks; recount S from the piece size so every
             // piece is non-empty ((S - 1) * kb_per < num_kb)
             args.kb_per = (args.num_kb + S - 1) / S;
             const int S2 = (args.num_kb + args.kb_per - 1) / args.kb_per;
             args.ksplit = S2;
+            // promotion inside short pieces: at least two chunks per piece, so
+            // the sign-centred plan (leading chunks of kc/2, then kc) still
+            // centres part of every piece (pieces of 4 K-blocks at kc = 4
+            // would be single chunks)
+            if (args.kc < args.num_kb && args.kc > 1 && args.kb_per < 2 * args.kc) {
+                args.kc = std::max(1, args.kb_per / 2);
+                set_center();
+            }
         }
         if (args.ksplit > 1) {
             const int S = args.ksplit;
@@ -594,7 +621,7 @@ static int choose_cta_group(int64_t n, int64_t pc, int num_kb, bool splitk_ok) {
         const int64_t tm = 128 * cg, tn = cg == 2 ? 256 : 128;
         const int64_t tiles = ((n + tm - 1) / tm) * ((pc + tn - 1) / tn);
         const int64_t slots = g_state.sms / cg;
-        const int S = splitk_ok ? splitk_factor(tiles, slots, num_kb) : 1;
+        const int S = splitk_ok ? splitk_factor(tiles, slots, num_kb, cg, true) : 1;
         const int64_t items = tiles * S;
         const int64_t kb_item = (num_kb + S - 1) / S;
         const double waves = (double)((items + slots - 1) / slots);

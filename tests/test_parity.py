@@ -125,7 +125,8 @@ def test_run_to_run_bitwise(la):
     assert torch.equal(C1, C2)
 
 
-def test_launch_count_and_stream(la):
+def test_launch_count_and_stream(la, monkeypatch):
+    monkeypatch.setenv("LA_SPLIT_K", "0")          # 256^3 splits K otherwise (+1 reduce launch)
     A, B = inputs.pair(256, 256, 256, "integer", device="cuda")
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
