@@ -43,9 +43,12 @@
  *    (==) on integer-valued inputs whose partial sums stay below 2^24.
  *    Measured envelope against the EXACT product (DESIGN.md section 4,
  *    units of 2^-20 * sum|a||b|, automatic promotion interval): random signs
- *    <= 0.66 at every K tested; same-sign inputs 0.54-0.93 once K spans >= 8
- *    promotion chunks (K >= 1024: sign-centred chunks), up to 1.7 for shorter
- *    K (K = 64 .. 512, where Listing 1 itself is 0.57-1.4 off).
+ *    <= 0.7 at every K tested; same-sign and other structured inputs
+ *    (scripts/fuzz_structured.py, ~1900 random shapes) <= 1.23 once K spans >= 8
+ *    promotion chunks (K >= 1024: sign-centred chunks; <= 0.93 for 256-wide
+ *    outputs) where Listing 1 itself is up to 7.6 off, and up to 1.6 for
+ *    shorter K where Listing 1 is up to 1.4 off -- always within the oracle's
+ *    own error + 2^-20 * sum (reading C14').
  *  - Deterministic: the same call on the same inputs gives the same bits
  *    (split-K partials are reduced in piece order).
  *  - LA_MODE_TF32: one pass on hi only; contract 2^-9 * sum_r |a_ir||b_rj|.
