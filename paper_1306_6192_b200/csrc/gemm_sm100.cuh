@@ -95,7 +95,7 @@ struct GemmArgs {
     int32_t sync_kb;    // K-blocks between arrival barriers (>= num_kb: once per tile)
     int32_t wave_slots; // counters in wave_sync; wave_sync[wave_slots] is the give-up flag
     int32_t debug;      // diagnostics only (results are garbage): 1 = skip TMA loads, 2 = skip MMAs
-    int64_t *trace;     // diagnostics only: per-CTA globaltimer stamps (8 per CTA), or nullptr
+    int64_t *trace;     // diagnostics only: per-CTA globaltimer stamps + MMA wait cycles (TRACE_SLOTS), or nullptr
     // 1: plain row-major output (cstride 1, no half rows, no gather) stored by
     // TMA through the kernel's tm_c map {p, n, ksplit} (C, or the split-K
     // partial slices); 0: per-thread stores (store_piece)
@@ -128,11 +128,12 @@ static __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *
     }
 }
 
+constexpr int TRACE_SLOTS = 10;  // 8 timestamps + the MMA warp's wait cycles (tempty, full)
 __device__ __forceinline__ void trace_stamp(int64_t *trace, int k) {
     if (trace == nullptr) return;
     int64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    trace[blockIdx.x * 8 + k] = t;
+    trace[blockIdx.x * TRACE_SLOTS + k] = t;
 }
 
 // Same, four elements per thread (count % 4 == 0, 16-byte aligned buffers).
@@ -480,6 +481,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int s = 0;
         uint32_t ph = 0, buf = 0, aph = 0;
         bool traced_mma = false;
+        int64_t wait_tempty = 0, wait_full = 0;  // diagnostics (args.trace): cycles the MMA warp waited
         for (int t = cluster_id; t < num_items; t += num_clusters) {
             const uint32_t idesc = t < args.full_items ? idesc_full : idesc_half;
             int tm_, tn_, part_, kb0, kb1, ks_;
@@ -492,12 +494,18 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 // sign-centred chunks accumulate onto the offset the epilogue
                 // preloaded into the buffer
                 const bool preloaded = plan.sc && ci >= 2;
+                const int64_t w0 = args.trace ? clock64() : 0;
                 if (chunk_first) {
                     if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[buf], aph ^ 1);
                     else ptx::mbar_wait(&tempty[buf], aph ^ 1);
                     ptx::tc_fence_after();
                 }
+                const int64_t w1 = args.trace ? clock64() : 0;
                 ptx::mbar_wait(&full[s], ph);
+                if (args.trace) {
+                    wait_tempty += w1 - w0;
+                    wait_full += clock64() - w1;
+                }
                 if (lane == 0 && kb == kb0 && !traced_mma) { trace_stamp(args.trace, 3); traced_mma = true; }
                 ptx::tc_fence_after();
                 {
@@ -539,6 +547,10 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
         }
         if (lane == 0) trace_stamp(args.trace, 4);
+        if (args.trace && lane == 0) {
+            args.trace[blockIdx.x * TRACE_SLOTS + 8] = wait_tempty;
+            args.trace[blockIdx.x * TRACE_SLOTS + 9] = wait_full;
+        }
     }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));

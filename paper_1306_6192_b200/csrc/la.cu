@@ -489,8 +489,8 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
     static int64_t *trace_buf = nullptr;
     const bool trace_on = diag_knob("LA_DIAG_TRACE", 0) != 0;
     if (trace_on) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 8 * sizeof(int64_t) * 1024);
-        cudaMemsetAsync(trace_buf, 0, 8 * sizeof(int64_t) * 1024, st);
+        if (!trace_buf) cudaMalloc(&trace_buf, TRACE_SLOTS * sizeof(int64_t) * 1024);
+        cudaMemsetAsync(trace_buf, 0, TRACE_SLOTS * sizeof(int64_t) * 1024, st);
         args.trace = trace_buf;
     }
 #else
@@ -550,11 +550,11 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
 #ifdef LA_DIAGNOSTICS
     if (args.trace) {
         const int nb = clusters * CG;
-        std::vector<int64_t> h((size_t)nb * 8);
+        std::vector<int64_t> h((size_t)nb * TRACE_SLOTS);
         cudaStreamSynchronize(st);
         cudaMemcpy(h.data(), args.trace, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost);
         int64_t t0s = INT64_MAX;
-        for (int b = 0; b < nb; b++) if (h[b * 8]) t0s = std::min(t0s, h[b * 8]);
+        for (int b = 0; b < nb; b++) if (h[b * TRACE_SLOTS]) t0s = std::min(t0s, h[b * TRACE_SLOTS]);
         static const char *names[8] = {"entry", "setup done", "producer past griddepcontrol.wait",
                                        "MMA: first stage full", "MMA: last commit", "epilogue: first chunk ready",
                                        "epilogue: stores done", "exit sync done"};
@@ -562,11 +562,18 @@ static la_status launch_gemm(int64_t n, int64_t m, int64_t j0, int64_t pc, const
                 (long long)n, (long long)pc, args.num_kb, args.kc, args.ksplit);
         for (int k = 0; k < 8; k++) {
             std::vector<double> v;
-            for (int b = 0; b < nb; b++) if (h[b * 8 + k]) v.push_back((h[b * 8 + k] - t0s) * 1e-3);
+            for (int b = 0; b < nb; b++) if (h[b * TRACE_SLOTS + k]) v.push_back((h[b * TRACE_SLOTS + k] - t0s) * 1e-3);
             if (v.empty()) continue;
             std::sort(v.begin(), v.end());
             fprintf(stderr, "la_diag_trace %-36s min %9.2f med %9.2f max %9.2f (%zu CTAs)\n", names[k], v.front(),
                     v[v.size() / 2], v.back(), v.size());
+        }
+        for (int k = 8; k < 10; k++) {
+            std::vector<double> v;
+            for (int b = 0; b < nb; b += CG) v.push_back((double)h[b * TRACE_SLOTS + k]);
+            std::sort(v.begin(), v.end());
+            fprintf(stderr, "la_diag_trace MMA warp waited on %-8s cycles: min %.0f med %.0f max %.0f (%zu CTAs)\n",
+                    k == 8 ? "tempty" : "full", v.front(), v[v.size() / 2], v.back(), v.size());
         }
     }
 #endif
