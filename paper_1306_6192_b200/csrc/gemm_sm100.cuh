@@ -481,7 +481,9 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int s = 0;
         uint32_t ph = 0, buf = 0, aph = 0;
         bool traced_mma = false;
-        int64_t wait_tempty = 0, wait_full = 0;  // diagnostics (args.trace): cycles the MMA warp waited
+#ifdef LA_DIAGNOSTICS
+        int64_t wait_tempty = 0, wait_full = 0;  // cycles the MMA warp waited (LA_DIAG_TRACE)
+#endif
         for (int t = cluster_id; t < num_items; t += num_clusters) {
             const uint32_t idesc = t < args.full_items ? idesc_full : idesc_half;
             int tm_, tn_, part_, kb0, kb1, ks_;
@@ -494,18 +496,24 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 // sign-centred chunks accumulate onto the offset the epilogue
                 // preloaded into the buffer
                 const bool preloaded = plan.sc && ci >= 2;
+#ifdef LA_DIAGNOSTICS
                 const int64_t w0 = args.trace ? clock64() : 0;
+#endif
                 if (chunk_first) {
                     if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[buf], aph ^ 1);
                     else ptx::mbar_wait(&tempty[buf], aph ^ 1);
                     ptx::tc_fence_after();
                 }
+#ifdef LA_DIAGNOSTICS
                 const int64_t w1 = args.trace ? clock64() : 0;
+#endif
                 ptx::mbar_wait(&full[s], ph);
+#ifdef LA_DIAGNOSTICS
                 if (args.trace) {
                     wait_tempty += w1 - w0;
                     wait_full += clock64() - w1;
                 }
+#endif
                 if (lane == 0 && kb == kb0 && !traced_mma) { trace_stamp(args.trace, 3); traced_mma = true; }
                 ptx::tc_fence_after();
                 {
@@ -547,10 +555,12 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
         }
         if (lane == 0) trace_stamp(args.trace, 4);
+#ifdef LA_DIAGNOSTICS
         if (args.trace && lane == 0) {
             args.trace[blockIdx.x * TRACE_SLOTS + 8] = wait_tempty;
             args.trace[blockIdx.x * TRACE_SLOTS + 9] = wait_full;
         }
+#endif
     }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
