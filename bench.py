@@ -276,24 +276,37 @@ def run_ours(a, rank, world, local_rank):
         comm = {"ncclCommCount": nr, "rank0_user_rank": crank, "backend": "nccl (library communicator)"}
         gather = {}
         for kind in ("nccl", "fused"):
-            Cf = la.gather_buffer(n, p) if kind == "fused" else torch.empty(n, p, device="cuda")
-            for _ in range(max(1, min(a.warmup, 2))):
-                la.gemm_multi(n, m, p, A, B, C, Cf, root=0, ngpu=world, stream=stream)
-            torch.cuda.synchronize()
-            dist.barrier()
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            for _ in range(a.steps):
-                la.gemm_multi(n, m, p, A, B, C, Cf, root=0, ngpu=world, stream=stream)
-            g1.record(stream)
-            torch.cuda.synchronize()
-            gt = torch.tensor([g0.elapsed_time(g1) / a.steps], device="cuda")
+            # the main line above is already measured: a failing gather variant
+            # is reported in its row instead of losing the line (every rank
+            # agrees on success before the next variant)
+            err = ""
+            try:
+                Cf = la.gather_buffer(n, p) if kind == "fused" else torch.empty(n, p, device="cuda")
+                for _ in range(max(1, min(a.warmup, 2))):
+                    la.gemm_multi(n, m, p, A, B, C, Cf, root=0, ngpu=world, stream=stream)
+                torch.cuda.synchronize()
+                dist.barrier()
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                for _ in range(a.steps):
+                    la.gemm_multi(n, m, p, A, B, C, Cf, root=0, ngpu=world, stream=stream)
+                g1.record(stream)
+                torch.cuda.synchronize()
+                gms = g0.elapsed_time(g1) / a.steps
+                del Cf
+            except Exception as ex:  # noqa: BLE001 -- reported, not fatal
+                err, gms = f"{type(ex).__name__}: {ex}"[:300], float("nan")
+            ok = torch.tensor([0.0 if err else 1.0], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            gt = torch.tensor([0.0 if err else gms], device="cuda")
             dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+            if ok.item() < 1.0:
+                gather[kind] = {"error": err or "failed on another rank"}
+                break
             gms = float(gt.item())
             gather[kind] = {"ms_per_step": gms, "value": flops / (gms * 1e-3) / 1e12, "unit": "TFLOP/s",
                             "api": "la_gemm_multi + " + ("ncclAllGather" if kind == "nccl" else
                                                          "fused epilogue stores into la_gather_alloc C_full")}
-            del Cf
 
     # roofline of the dominant kernel (the GEMM), per launch, this rank
     pk, src = _peaks()
