@@ -25,9 +25,12 @@
 // bias that grows with the number of MMAs per accumulator (3.1 x 2^-20 S at
 // K=16384).  So the MMA warp accumulates `kc` K-blocks per TMEM chunk and the
 // epilogue adds every chunk into an fp32 round-to-nearest register running
-// sum (0.06 x 2^-20 S at chunks of 256; the host picks 64 / 128 / 256 by K,
-// because one long chunk's truncations do not average out).  Two TMEM
-// accumulator buffers let the epilogue of chunk c overlap the MMAs of c+1.
+// sum (0.06 x 2^-20 S at chunks of 256 on random signs; the host picks 32 /
+// 64 / 128 by K, because one long chunk's truncations do not average out).
+// Two TMEM accumulator buffers let the epilogue of chunk c overlap the MMAs of
+// c+1.  Same-sign sums would still drift toward zero chunk by chunk, so chunks
+// are sign-centred (ChunkPlan; the epilogue preloads an offset of the other
+// sign into the buffer of chunk c+2).
 //
 // CG == 1: one CTA computes a 128 x BN tile (UMMA M=128).
 // CG == 2: a cluster of two CTAs (a CTA pair on one TPC) computes a 256 x BN
