@@ -61,7 +61,8 @@ la_status fail(la_status s, const char *fmt, ...);
 //                          C_full copies at float offsets 0, s, 2s.. of its own
 //                          window (tests/test_multi.py)
 // Experiment knobs (LA_SPLIT_T32, LA_GROUP_M, LA_WAVE_SYNC, LA_HOST_TAIL_SPLIT,
-// LA_HOST_TRACE, LA_DIAG_CLUSTERS, LA_DIAG_TRACE, LA_DEBUG_KERNEL) are read only
+// LA_HOST_TRACE, LA_DIAG_CLUSTERS, LA_DIAG_TRACE, LA_DEBUG_KERNEL,
+// LA_SPLITK_MIN_PIECE1) are read only
 // in the diagnostics build (LA_BUILD_DIAGNOSTICS=1); elsewhere diag_knob
 // returns the default.
 int64_t test_hook(const char *name, int64_t dflt);
