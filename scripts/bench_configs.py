@@ -72,8 +72,8 @@ def time_graph(A, B, C, calls=20, reps=5):
 
 def main():
     la.init(0)
-    print("| config | mode | median ms (events per call) | min ms | graph ms/call | logical TFLOP/s | % TF32 datasheet (issued) | max err / (2^-20 S) | integer exact | oracle (host) |")
-    print("|---|---|---|---|---|---|---|---|---|---|")
+    print("| config | mode | median ms (events per call) | min ms | graph ms/call | logical TFLOP/s | % TF32 datasheet (issued) | max err / (2^-20 S) | integer exact | oracle (host) | oracle 1 thread | speedup vs oracle, 1 thr / all thr (Table 2 style) |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for label, n, m, p, modes, full in CONFIGS:
         A, B = inputs.pair(n, m, p, "stress", device="cuda")
         C = torch.empty(n, p, device="cuda")
@@ -92,6 +92,19 @@ def main():
         frac = (len(rows) * len(cols)) / (n * p)
         oracle_note = (f"{t_or:.2f} s full, {THREADS} thr" if full else
                        f"{t_or / frac:.0f} s extrapolated from {len(rows)}x{len(cols)} sample, {THREADS} thr")
+        t_all = t_or / frac
+        # single thread: full up to C2, else a 16 x 16 sample extrapolated
+        if full:
+            t0 = time.perf_counter()
+            oracle.gemm(As, Bs, threads=1)
+            t_one = time.perf_counter() - t0
+            one_note = f"{t_one:.2f} s full"
+        else:
+            r1, c1 = rows[:16], cols[:16]
+            t0 = time.perf_counter()
+            oracle.gemm(As[:16], Bs[:, :16], threads=1)
+            t_one = (time.perf_counter() - t0) * (n * p) / (len(r1) * len(c1))
+            one_note = f"{t_one:.0f} s extrapolated from 16x16"
         Ai, Bi = inputs.pair(n, m, p, "integer", device="cuda")
         Ci = la.gemm(Ai, Bi)
         Ais = inputs.generate(n, m, 0, "integer", row_idx=rows).numpy()
@@ -107,8 +120,10 @@ def main():
             passes = 3 if mode == "3xtf32" else 1
             tf = 2.0 * n * m * p / ((gms if gms else med) * 1e-3) / 1e12
             gcol = f"{gms:.4f}" if gms else "-"
+            t_gpu = (gms if gms else med) * 1e-3
             print(f"| {label} | {mode} | {med:.3f} | {mn:.3f} | {gcol} | {tf:.1f} | {100 * passes * tf / TF32_PEAK:.1f} | "
-                  f"{err:.3f} | {int_ok if mode == '3xtf32' else '-'} | {oracle_note} |", flush=True)
+                  f"{err:.3f} | {int_ok if mode == '3xtf32' else '-'} | {oracle_note} | {one_note} | "
+                  f"{t_one / t_gpu:,.0f} / {t_all / t_gpu:,.0f} |", flush=True)
         la.set_mode("3xtf32")
 
 
