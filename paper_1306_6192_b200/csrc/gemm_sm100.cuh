@@ -244,20 +244,6 @@ struct ChunkPlan {
         const int s0 = start(j);
         return min(j < 2 ? f : kc, nkb - s0);
     }
-    // K-block rel of the item: its chunk and whether it opens / closes it
-    __device__ __forceinline__ void at(int rel, int &ci, bool &first, bool &last) const {
-        if (rel < 2 * f) {
-            ci = rel / f;
-            first = rel % f == 0;
-            last = rel % f == f - 1;
-        } else {
-            const int r2 = rel - 2 * f;
-            ci = 2 + r2 / kc;
-            first = r2 % kc == 0;
-            last = r2 % kc == kc - 1;
-        }
-        last = last || rel == nkb - 1;
-    }
 };
 
 // Work item w -> tile (tm, tn), part (-1 = whole tile, 0/1 = column half) and
@@ -492,10 +478,12 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             int tm_, tn_, part_, kb0, kb1, ks_;
             decode_item(t, args, tm_, tn_, part_, kb0, kb1, ks_);
             const ChunkPlan plan(kb1 - kb0, kc, args.center_kb > 0);
+            // walk the chunk plan incrementally (no division in the issue loop:
+            // with one TF32 pass a K-block is only 4 MMAs of 128 cycles)
+            int ci = 0, left = plan.len(0);  // current chunk, K-blocks left in it
+            bool chunk_first = true;
             for (int kb = kb0; kb < kb1; kb++) {
-                int ci;
-                bool chunk_first, chunk_last;
-                plan.at(kb - kb0, ci, chunk_first, chunk_last);
+                const bool chunk_last = left == 1;
                 // sign-centred chunks accumulate onto the offset the epilogue
                 // preloaded into the buffer
                 const bool preloaded = plan.sc && ci >= 2;
@@ -550,9 +538,14 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     if (chunk_last) ptx::mma_commit_elect<CG>(&tfull[buf]);
                 }
                 __syncwarp();
+                chunk_first = chunk_last;
                 if (chunk_last) {
                     buf ^= 1;
                     if (buf == 0) aph ^= 1;
+                    ++ci;
+                    left = kb + 1 < kb1 ? plan.len(ci) : 0;
+                } else {
+                    --left;
                 }
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
