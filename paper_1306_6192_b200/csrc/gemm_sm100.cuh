@@ -623,11 +623,15 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 // written into the buffer for chunk c+2, which the MMA then
                 // accumulates onto: the partial sums start on the other side of
                 // zero and cross it, and truncations up and down cancel (0.96 x
-                // 2^-20 S at K = 16384).  Drained values are x = R - off; mixed
+                // 2^-20 S at K = 16384).  Chunk values are x = R - off; mixed
                 // signs give off = 0 and the same bits as plain promotion.  Exact
                 // on integer data: off is half an integer chunk sum and |R| <= |x|.
                 float acc[Cfg::PIECES][32];
                 float off_cur = 0.0f, off_oth = 0.0f;  // offsets preloaded in this / the other buffer
+                // the drained values R = off + x are summed as they are and the
+                // offsets (one per row) subtracted once at the end: one FADD per
+                // element per chunk instead of two (off_sum = 0 on mixed signs)
+                float off_sum = 0.0f;
 #pragma unroll 1
                 for (int c = 0; c < nchunks; c++) {
                     ptx::mbar_wait(&tfull[buf], aph);
@@ -655,10 +659,10 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                                 }
                             } else {
 #pragma unroll
-                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v0[i]) - off_cur;
+                                for (int i = 0; i < 32; i++) acc[qq][i] += __uint_as_float(v0[i]);
                                 if (two) {
 #pragma unroll
-                                    for (int i = 0; i < 32; i++) acc[qq + 1][i] += __uint_as_float(v1[i]) - off_cur;
+                                    for (int i = 0; i < 32; i++) acc[qq + 1][i] += __uint_as_float(v1[i]);
                                 }
                             }
                             if (refill) {
@@ -700,6 +704,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     if (lane == 0) ptx::mbar_arrive_cta0<CG>(&tempty[buf]);
                     buf ^= 1;
                     if (buf == 0) aph ^= 1;
+                    off_sum += off_cur;
                     off_cur = off_oth;
                     off_oth = off_new;
                 }
@@ -708,7 +713,7 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     if (qq < pieces) {
                         uint32_t v[32];
 #pragma unroll
-                        for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i]);
+                        for (int i = 0; i < 32; i++) v[i] = __float_as_uint(acc[qq][i] - off_sum);
                         put(col0 + qq * 32, v);
                     }
                 }
