@@ -665,7 +665,9 @@ __global__ void __cluster_dims__(CG, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                                     for (int i = 0; i < 32; i++) acc[qq + 1][i] += __uint_as_float(v1[i]);
                                 }
                             }
-                            if (refill) {
+                            // (once this row's values have shown both signs the offset
+                            // is 0 whatever follows: skip the rest of the scan)
+                            if (refill && !(lo < off_cur && hi > off_cur)) {
 #pragma unroll
                                 for (int i = 0; i < 32; i++) {
                                     lo = fminf(lo, __uint_as_float(v0[i]));
