@@ -45,7 +45,7 @@
  *    units of 2^-20 * sum|a||b|, automatic promotion interval): random signs
  *    <= 0.7 at every K tested; same-sign and other structured inputs
  *    (scripts/fuzz_structured.py, ~1900 random shapes) <= 1.23 once K spans >= 8
- *    promotion chunks (K >= 1024: sign-centred chunks; <= 0.93 for 256-wide
+ *    promotion chunks (K >= 1024: sign-centred chunks; <= 0.85 for 256-wide
  *    outputs) where Listing 1 itself is up to 7.6 off, and up to 1.6 for
  *    shorter K where Listing 1 is up to 1.4 off -- always within the oracle's
  *    own error + 2^-20 * sum (reading C14').
