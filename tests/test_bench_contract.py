@@ -1,6 +1,6 @@
 """bench.py's JSON-line contract, checked without a GPU: the reference arm
 runs here (the oracle on the host cores), and the committed GPU line
-(profiles/bench_r02d.json, the final round-2 line) carries every key the driver reads."""
+(profiles/bench_r02e.json, the final round-2 line) carries every key the driver reads."""
 import json
 import os
 import subprocess
@@ -27,7 +27,7 @@ def test_reference_arm_line():
 
 
 def test_committed_gpu_line_has_every_key():
-    line = json.load(open(os.path.join(ROOT, "profiles", "bench_r02d.json")))
+    line = json.load(open(os.path.join(ROOT, "profiles", "bench_r02e.json")))
     assert BASE_KEYS <= set(line)
     assert line["n_gpus"] == 1 and line["warmup"] >= 3
     assert line["config"]["workload"] and "l2" in line["config"]
