@@ -79,6 +79,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
 
 // 2-D fp32 tensor map over a rows x cols row-major buffer (cols % 4 == 0),
 // box = box_rows x 32 columns, 128-byte swizzle, OOB elements read as zero.
+// L2 promotion of 128 B (one swizzle row): n = 4096 0.552 vs 0.555 ms with
+// 256 B, equal at 16384 (scripts/ab_raw.py).
 static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols,
                            int box_rows, int box_k = BK) {
     auto enc = get_encoder();
@@ -90,7 +92,7 @@ static la_status make_tmap(CUtensorMap *map, const float *ptr, int64_t rows, int
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides,
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(LA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld", (int)r,
                     (long long)rows, (long long)cols);
