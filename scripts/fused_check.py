@@ -3,7 +3,12 @@
 separate split pass: bitwise equality on integer and random inputs over a few
 shapes (small first), the oracle on the small ones, then timings of both paths.
 
-    python scripts/fused_check.py [--quick]
+Kept for the record of profiles/fused_split_r02.md: it drives LA_FUSED_SPLIT,
+which exists only in the experiment's commit ("Experiment: operand split fused
+into the GEMM ..."); the fused path was removed in the next commit, so on
+later builds both arms run the split pass.
+
+    python scripts/fused_check.py [--quick|--probe|--debug-split]
 """
 import os
 import sys
