@@ -1,10 +1,13 @@
-"""bench.py's JSON-line contract, checked without a GPU: the reference arm
-runs here (the oracle on the host cores), and the committed GPU line
-(profiles/bench_r02e.json, the final round-2 line) carries every key the driver reads."""
+"""bench.py's JSON-line contract.  Without a GPU: the reference arm runs here
+(the oracle on the host cores), the committed GPU line (profiles/bench_r02e.json,
+the final round-2 line) carries every key the driver reads, and an N-GPU
+request is never timed on fewer GPUs.  On a GPU (-m gpu): a small live run."""
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -68,3 +71,26 @@ def test_reference_arm_reports_requested_gpus():
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1])["n_gpus"] == 4
+
+
+@pytest.mark.gpu
+def test_live_gpu_line_small():
+    """bench.py on the GPU (small n so it takes seconds): one JSON line with
+    every key the driver reads, our kernels counted in the timed region, the
+    roofline of the GEMM kernel measured live and an e2e number through the
+    host-buffer API."""
+    import pytest
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    r = subprocess.run([sys.executable, "bench.py", "--n", "2048", "--steps", "3", "--warmup", "3",
+                        "--cpu-seconds", "1"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert BASE_KEYS <= set(line) and line["n_gpus"] == 1 and line["value"] > 0
+    assert line["gpu_launches"] > 0
+    rf = line["roofline"]
+    assert rf["bound"] == "tensor" and 0 < rf["frac"] <= 1.5 and rf["achieved"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 2 * 4 * 2048 ** 2
+    assert line["cpu_baseline"]["kind"] == "oracle"
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
