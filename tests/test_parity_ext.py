@@ -76,6 +76,19 @@ def test_cgemm_parity(la, kind, n, m, p):
     _ccheck(A, B, C, kind)
 
 
+@pytest.mark.parametrize("n,m,p", [(128, 4096, 128), (200, 2500, 96)])
+def test_cgemm_same_sign_integer_exact(la, n, m, p):
+    """Non-negative integer real and imaginary parts: the imaginary rows of the
+    real embedding are same-sign sums, where sign-centred promotion chunks
+    preload offsets (K spans >= 8 chunks here); integer partial sums stay
+    exact, so the product equals the complex Listing 1 value for value."""
+    A, B = _cgen(n, m, "integer", 0), _cgen(m, p, "integer", 1)
+    A = torch.complex(A.real.abs(), A.imag.abs())
+    B = torch.complex(B.real.abs(), B.imag.abs())
+    C = la.cgemm(A.cuda(), B.cuda()).cpu().numpy()
+    _ccheck(A, B, C, "integer")
+
+
 def test_cgemm_4096_sampled(la):
     n = 4096
     A, B = _cgen(n, n, "random", 0, "cuda"), _cgen(n, n, "random", 1, "cuda")
